@@ -1,0 +1,252 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * staleflow train-math C-ABI — the per-token training-math hot path of Relax
+ * (arXiv 2604.11554) on B200 (sm_100a).
+ *
+ * This header is the drop-in boundary. The reference (`/root/reference/proj`)
+ * models this compute as synthetic latency at its role-compute seams; every
+ * entry point below names the seam it replaces:
+ *
+ *   - Actor loss fwd+bwd ........ trainer_compute_batch  proj/src/sim_runtime.cpp:431-463
+ *                                 (latency draw at :441, draw_train_micro :142-145)
+ *                                 trainer_thread         proj/src/wall_runtime.cpp:136-232
+ *                                 (sleep_units at :174 and :197)
+ *   - ActorFwd / RefLogP stages . stage_run_batch        proj/src/sim_runtime.cpp:304-350
+ *                                 (payload stub :328-333), stage_thread wall_runtime.cpp:103-134
+ *                                 (sleep at :118, stub payload :126-129); field contract
+ *                                 controller.cpp:76-77 ("logp", "ref_logp")
+ *   - Advantages stage .......... same seams, field "reward" -> "advantage" (controller.cpp:79)
+ *   - R3 routing replay ......... a new data-declared field (config.cpp:127-148); paper §5.5
+ *
+ * Conventions (mirroring proj/include/staleflow/result.hpp:14-47 and :62-63):
+ *   - every function returns an int that is static_cast<uint16_t>(staleflow::Errc):
+ *       0  = Ok
+ *       21 = ConfigError  (bad shape, dtype, pointer, alignment or parameter)
+ *       26 = Internal     (CUDA launch / runtime failure)
+ *     the message for the last failure on a handle is in sf_tm_last_error().
+ *     No C++ exception crosses this ABI.
+ *   - all device pointers are caller-owned; the handle owns only scratch
+ *     (grown once, reused; no allocation in a steady-state call).
+ *   - every call is stream-ordered and asynchronous on `stream`
+ *     (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - handles are thread-compatible: one handle per role thread, or external
+ *     synchronisation (the reference runs one thread per role,
+ *     wall_runtime.cpp:296-315).
+ *
+ * The math (decisions P1-P9 of SURVEY.md §8) is pinned in DESIGN.md §2 and
+ * restated in fp64 by oracle/sf_oracle.c.
+ */
+#ifndef STALEFLOW_TRAIN_MATH_H_
+#define STALEFLOW_TRAIN_MATH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_TM_ABI_VERSION 1
+
+/* Error codes: numerically identical to staleflow::Errc (result.hpp:14-47). */
+#define SF_TM_OK 0
+#define SF_TM_CONFIG_ERROR 21
+#define SF_TM_INTERNAL 26
+
+/* Element types of the V-wide logits / router-logit rows. */
+#define SF_TM_F32 0
+#define SF_TM_BF16 1
+
+/* Element types of recorded expert indices (R3). */
+#define SF_TM_IDX_I32 0
+#define SF_TM_IDX_U8 1
+
+/* GRPO group-std modes (decision P2/P3). */
+#define SF_TM_STD_UNBIASED 0   /* sample std, N-1 (veRL) */
+#define SF_TM_STD_POPULATION 1 /* N */
+#define SF_TM_STD_NONE 2       /* Dr.GRPO: A = r - mean */
+
+/* Loss normalisation modes. */
+#define SF_TM_NORM_TOKEN_MEAN 0     /* DAPO: 1 / sum(mask) over the launch  */
+#define SF_TM_NORM_SEQ_MEAN 1       /* GRPO: mean over seqs of token-means   */
+#define SF_TM_NORM_EXPLICIT 2       /* caller-supplied inv_norm (version-level N) */
+
+/* Masked-row contract for dlogits (decision P7). */
+#define SF_TM_MASKED_ZERO_FILL 0 /* dense: masked rows of dlogits are written as 0 */
+#define SF_TM_MASKED_SKIP 1      /* sparse: masked rows of dlogits are left untouched */
+
+/* Metrics written by the loss (device float[SF_TM_NUM_METRICS]); each is a
+ * w-weighted sum with w_t = mask_t * inv_norm_t, i.e. a masked token-mean
+ * under SF_TM_NORM_TOKEN_MEAN. */
+#define SF_TM_M_LOSS 0      /* sum w*(pg + beta*kl - ent_coef*H)         */
+#define SF_TM_M_PG 1        /* sum w*pg                                  */
+#define SF_TM_M_KL 2        /* sum w*kl_k3(ref || cur)                   */
+#define SF_TM_M_ENTROPY 3   /* sum w*H                                   */
+#define SF_TM_M_CLIPFRAC 4  /* sum w*[clipped]                           */
+#define SF_TM_M_RATIO 5     /* sum w*ratio                               */
+#define SF_TM_M_ACTIVE 6    /* number of loss-active tokens (w != 0)     */
+#define SF_TM_M_PPO_KL 7    /* sum w*(old_logp - logp)                   */
+#define SF_TM_NUM_METRICS 8
+
+typedef struct sf_tm_handle* sf_tm_t;
+
+typedef struct sf_tm_loss_params {
+  float clip_eps_low;    /* P4: 0.2                                  */
+  float clip_eps_high;   /* P4: 0.28 (DAPO clip-higher)              */
+  float dual_clip_c;     /* P4: 0 = off, else > 1 (e.g. 3)           */
+  float kl_beta;         /* P5: 0 = pure DAPO                         */
+  float entropy_coef;    /* P6: 0 = entropy is a metric only          */
+  float inv_temperature; /* P1: 1/tau, 1.0 = no temperature           */
+  int32_t norm_mode;     /* SF_TM_NORM_*                              */
+  float inv_norm;        /* used when norm_mode == SF_TM_NORM_EXPLICIT */
+  int32_t masked_rows;   /* SF_TM_MASKED_*                            */
+  int32_t reserved;
+} sf_tm_loss_params;
+
+/* Fills the DAPO defaults above (eps 0.2/0.28, no dual clip, beta 0,
+ * ent 0, tau 1, token-mean, zero-fill). */
+void sf_tm_default_loss_params(sf_tm_loss_params* p);
+
+/* ---- handle ------------------------------------------------------------ */
+int sf_tm_create(int device, sf_tm_t* out);
+int sf_tm_destroy(sf_tm_t h);
+const char* sf_tm_last_error(sf_tm_t h);
+int sf_tm_abi_version(void);
+/* Number of kernel launches issued on this handle since creation (evidence for
+ * the bench's gpu_launches count). */
+uint64_t sf_tm_launch_count(sf_tm_t h);
+
+/* ---- a6: varlen packing metadata --------------------------------------
+ * seq_lens[B] (>= 0), prompt_lens[B] (optional; tokens [0, prompt_len) of a
+ * sequence are loss-masked), group_ids[B] (optional).
+ * Out: cu_seqlens[B+1] (exclusive scan, int32), seq_id[T] (optional),
+ * mask[T] u8 (optional, needs prompt_lens or gives all-ones), tok_group[T]
+ * (optional, needs group_ids). T = sum(seq_lens) must be passed and match.
+ * Bit-exact against the oracle. Anchor: MicroBatch per-sample keys
+ * types.hpp:48-59; packing is a reference non-goal. */
+int sf_tm_varlen_meta(sf_tm_t h, const int32_t* seq_lens, const int32_t* prompt_lens,
+                      const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,
+                      int32_t* seq_id, uint8_t* mask, int32_t* tok_group, void* stream);
+
+/* ---- a3: GRPO group advantage ------------------------------------------
+ * A_i = (r_i - mean_g(i)) / (std_g(i) + eps); groups keyed by arbitrary int32
+ * ids (need not be contiguous: the bus delivers in readiness order,
+ * transfer_queue.cpp:162-175). Groups whose rewards are all equal give A = 0
+ * exactly (P3). Optional out_group_size[B] (int32, bit-exact).
+ * Replaces the Advantages stage stub (controller.cpp:79, sim_runtime.cpp:304-350). */
+int sf_tm_grpo_advantage(sf_tm_t h, const float* rewards, const int32_t* group_ids, int64_t B,
+                         float eps, int32_t std_mode, float* out_adv, int32_t* out_group_size,
+                         void* stream);
+
+/* ---- a1: fused log-softmax gather, forward only -------------------------
+ * logits[T, V] row stride ld (elements), dtype SF_TM_F32 / SF_TM_BF16;
+ * targets[T] in [0, V). Out (each optional): logp[T], entropy[T], lse[T] fp32.
+ * One HBM pass (2V or 4V bytes/token). Producer of the "logp"/"ref_logp"
+ * fields (controller.cpp:76-77). */
+int sf_tm_logprob_fwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                      int64_t ld, const int32_t* targets, float inv_temperature, float* out_logp,
+                      float* out_entropy, float* out_lse, void* stream);
+
+/* ---- a4 prologue: per-token advantage and loss weight --------------------
+ * From cu_seqlens[B+1], adv_seq[B], mask[T] (u8, NULL = all active):
+ * out_adv_tok[T] = adv_seq[seq(t)], out_w_tok[T] = mask_t * inv_norm_t. */
+int sf_tm_token_weights(sf_tm_t h, const int32_t* cu_seqlens, int64_t B, const float* adv_seq,
+                        const uint8_t* mask, int64_t T, int32_t norm_mode, float inv_norm,
+                        float* out_adv_tok, float* out_w_tok, void* stream);
+
+/* ---- a1+a4+a2: the fused hot path ---------------------------------------
+ * Per token t with weight w_t (0 = masked) and advantage A_t:
+ *   logp, H from the logits row; ratio = exp(logp - old_logp);
+ *   pg = -min(ratio*A, clip(ratio, 1-eps_lo, 1+eps_hi)*A)  (+ dual clip);
+ *   kl = exp(ref - logp) - (ref - logp) - 1;  l = pg + beta*kl - ent_coef*H;
+ *   loss = sum_t w_t * l_t;  dlogits = d loss / d logits.
+ * adv_tok/w_tok come from sf_tm_token_weights. dlogits has the logits dtype,
+ * row stride ld_d; dlogits == logits (in place) is supported. out_metrics is
+ * device float[SF_TM_NUM_METRICS] (deterministic fixed-order reduction).
+ * out_logp / out_entropy optional. Replaces the trainer seam latency
+ * (sim_runtime.cpp:441, wall_runtime.cpp:197). */
+int sf_tm_pg_loss_fwd_bwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                          int64_t ld, const int32_t* targets, const float* old_logp,
+                          const float* ref_logp, const float* adv_tok, const float* w_tok,
+                          const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                          float* out_metrics, float* out_logp, float* out_entropy, void* stream);
+
+/* ---- whole trainer micro-batch from HOST buffers (the seam call) --------
+ * Copies the bus fields of one MicroBatch (types.hpp:48-59; trainer field set
+ * [advantage, logp, ref_logp, response, reward], controller.cpp:80) from host
+ * memory (pinned for async DMA), runs varlen meta -> GRPO advantage -> token
+ * weights -> fused loss fwd+bwd on device-resident logits (the LM-head output,
+ * which never crosses the bus), and copies the metrics back to h_metrics
+ * (valid after `stream` is synchronised).
+ *   h_targets[T], h_old_logp[T], h_ref_logp[T]: packed per-token fields;
+ *   h_seq_lens[B], h_prompt_lens[B] (optional), h_rewards[B], h_group_ids[B];
+ *   h_mask[T] (optional; overrides prompt_lens-derived mask).
+ * If adv_eps < 0 the rewards are taken as precomputed advantages. */
+int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                       int64_t ld, const int32_t* h_targets, const float* h_old_logp,
+                       const float* h_ref_logp, const uint8_t* h_mask, const int32_t* h_seq_lens,
+                       const int32_t* h_prompt_lens, const float* h_rewards,
+                       const int32_t* h_group_ids, int64_t B, float adv_eps, int32_t std_mode,
+                       const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                       float* h_metrics, void* stream);
+
+/* ---- a5: R3 rollout routing replay gate ---------------------------------
+ * router_logits[L*T, E] (dtype), rec_idx[L*T, k] (SF_TM_IDX_I32 / _U8).
+ * renorm = 1: w_j = softmax over the k recorded experts (P8, norm_topk_prob);
+ * renorm = 0: w_j = softmax over all E, gathered at the recorded experts.
+ * out_w[L*T, k] fp32; out_idx[L*T, k] int32 bit-exact copy of the replayed
+ * indices (optional); out_mismatch (optional, device uint32[L+1]): per layer
+ * the number of tokens whose trainer top-k set (ties -> lowest index, P9)
+ * differs from the recorded set, and the total in [L]. L = layers, rows are
+ * layer-major. */
+int sf_tm_r3_gate_fwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64_t L, int64_t T,
+                      int64_t E, int64_t k, const void* rec_idx, int32_t idx_dtype, int32_t renorm,
+                      float* out_w, int32_t* out_idx, uint32_t* out_mismatch, void* stream);
+
+/* Backward of sf_tm_r3_gate_fwd: given w (its output) and dw[L*T, k], writes
+ * dlogits[L*T, E] (router-logit dtype); non-recorded experts get 0 when
+ * renorm = 1. renorm = 0 re-reads router_logits. */
+int sf_tm_r3_gate_bwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64_t L, int64_t T,
+                      int64_t E, int64_t k, const void* rec_idx, int32_t idx_dtype, int32_t renorm,
+                      const float* w, const float* dw, void* dlogits, void* stream);
+
+/* ---- a7: vocab-parallel (logits sharded over P ranks by vocab) ----------
+ * Pass 1 (local): per-row partial stats of this rank's shard
+ * [vocab_start, vocab_start + Vp): out_stats[T*4] = {max z, sum e^(z-max),
+ * sum e^(z-max)(z-max), z_target or NaN if the target is not in the shard}.
+ * The caller all-gathers stats over ranks (NCCL) into gathered[P*T*4]. */
+int sf_tm_vp_partial_stats(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T,
+                           int64_t Vp, int64_t ld, int64_t vocab_start, const int32_t* targets,
+                           float inv_temperature, float* out_stats, void* stream);
+
+/* Pass 2: combine gathered stats of all P shards, compute the loss exactly as
+ * sf_tm_pg_loss_fwd_bwd (metrics are identical on every rank: each rank
+ * computes the full per-row scalars) and write this shard's dlogits. */
+int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T,
+                          int64_t Vp, int64_t ld, int64_t vocab_start, const float* gathered_stats,
+                          int32_t P, const int32_t* targets, const float* old_logp,
+                          const float* ref_logp, const float* adv_tok, const float* w_tok,
+                          const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                          float* out_metrics, float* out_logp, float* out_entropy, void* stream);
+
+/* ---- synthetic inputs (bench / tests) ------------------------------------
+ * Counter-based, seeded with the reference's SplitMix64 (rng.hpp:17-39)
+ * evaluated at element index: u_i = mix64(seed + (i+1)*0x9e3779b97f4a7c15),
+ * i.e. the i-th output of staleflow::SplitMix64(seed).
+ * Logits row t: N(0, sigma^2) (Box-Muller), plus a peak logit +U(peak_lo,
+ * peak_hi) at id peak_id[t] (optional), plus a fraction `outlier_frac` of
+ * entries set to +-30; rounded to the dtype. */
+int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,
+                       uint64_t seed, float sigma, const int32_t* peak_id, float peak_lo,
+                       float peak_hi, float outlier_frac, void* stream);
+
+/* ---- testing hook ---------------------------------------------------------
+ * on != 0 routes all row kernels to the generic two-pass (non-TMA) kernel so
+ * tests can cover both code paths; process-wide. Not for production use. */
+int sf_tm_debug_force_generic(int on);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STALEFLOW_TRAIN_MATH_H_ */

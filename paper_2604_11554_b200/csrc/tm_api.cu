@@ -1,0 +1,590 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// C-ABI layer of include/staleflow/train_math.h: argument validation, error
+// mapping onto staleflow::Errc (proj/include/staleflow/result.hpp:14-47: Ok=0,
+// ConfigError=21, Internal=26), handle-owned scratch, and the host-buffer
+// trainer-seam call sf_tm_pg_step_host. No exception crosses this boundary.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "staleflow/train_math.h"
+#include "tm_internal.h"
+
+struct sf_tm_handle {
+  int device = 0;
+  std::string err;
+  uint64_t launches = 0;
+  // metric partials for the deterministic row-kernel reduction
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  int max_partial_blocks = 0;
+  // token-weight scratch
+  int32_t* cnt = nullptr;
+  int64_t cnt_cap = 0;
+  unsigned* ticket2 = nullptr;
+  int64_t* tot = nullptr;
+  // sf_tm_pg_step_host scratch
+  int64_t tcap = 0, bcap = 0;
+  int32_t* d_targets = nullptr;
+  float* d_old = nullptr;
+  float* d_ref = nullptr;
+  uint8_t* d_mask = nullptr;
+  float* d_advtok = nullptr;
+  float* d_wtok = nullptr;
+  int32_t* d_lens = nullptr;
+  int32_t* d_plens = nullptr;
+  float* d_rewards = nullptr;
+  int32_t* d_gids = nullptr;
+  int32_t* d_cu = nullptr;
+  float* d_adv = nullptr;
+  int32_t* d_total = nullptr;
+  float* d_metrics = nullptr;
+};
+
+namespace {
+
+constexpr int kMaxPartialBlocks = 4096;
+
+int fail(sf_tm_t h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_fail(sf_tm_t h, int e, const char* where) {
+  if (e == -1) return fail(h, SF_TM_CONFIG_ERROR, std::string(where) + ": " + h->err);
+  const cudaError_t ce = static_cast<cudaError_t>(e);
+  return fail(h, SF_TM_INTERNAL,
+              std::string(where) + ": " + cudaGetErrorName(ce) + ": " + cudaGetErrorString(ce));
+}
+
+int check_cuda(sf_tm_t h, int e, const char* where) {
+  if (e == 0) return SF_TM_OK;
+  return cuda_fail(h, e, where);
+}
+
+int use_device(sf_tm_t h) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != h->device) {
+    const cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
+  }
+  return SF_TM_OK;
+}
+
+bool bad_dtype(int32_t d) { return d != SF_TM_F32 && d != SF_TM_BF16; }
+
+template <typename P>
+int grow(sf_tm_t h, P** p, int64_t n, const char* what) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (n <= 0) return SF_TM_OK;
+  const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), static_cast<size_t>(n) * sizeof(P));
+  if (e != cudaSuccess) return cuda_fail(h, e, what);
+  return SF_TM_OK;
+}
+
+int ensure_cnt(sf_tm_t h, int64_t B) {
+  if (B <= h->cnt_cap) return SF_TM_OK;
+  int64_t cap = B < 1024 ? 1024 : B;
+  int rc = grow(h, &h->cnt, cap, "scratch cnt");
+  if (rc) return rc;
+  h->cnt_cap = cap;
+  return SF_TM_OK;
+}
+
+int check_loss_params(sf_tm_t h, const sf_tm_loss_params* p) {
+  if (!p) return fail(h, SF_TM_CONFIG_ERROR, "params is NULL");
+  if (!(p->clip_eps_low >= 0.f && p->clip_eps_low < 1.f))
+    return fail(h, SF_TM_CONFIG_ERROR, "clip_eps_low must be in [0, 1)");
+  if (!(p->clip_eps_high >= 0.f && std::isfinite(p->clip_eps_high)))
+    return fail(h, SF_TM_CONFIG_ERROR, "clip_eps_high must be >= 0");
+  if (!(p->dual_clip_c == 0.f || p->dual_clip_c > 1.f))
+    return fail(h, SF_TM_CONFIG_ERROR, "dual_clip_c must be 0 (off) or > 1");
+  if (!std::isfinite(p->kl_beta) || !std::isfinite(p->entropy_coef))
+    return fail(h, SF_TM_CONFIG_ERROR, "kl_beta / entropy_coef must be finite");
+  if (!(p->inv_temperature > 0.f && std::isfinite(p->inv_temperature)))
+    return fail(h, SF_TM_CONFIG_ERROR, "inv_temperature must be > 0");
+  if (p->norm_mode < 0 || p->norm_mode > 2)
+    return fail(h, SF_TM_CONFIG_ERROR, "norm_mode must be SF_TM_NORM_*");
+  if (p->norm_mode == SF_TM_NORM_EXPLICIT && !(std::isfinite(p->inv_norm) && p->inv_norm >= 0.f))
+    return fail(h, SF_TM_CONFIG_ERROR, "inv_norm must be finite and >= 0");
+  if (p->masked_rows != SF_TM_MASKED_ZERO_FILL && p->masked_rows != SF_TM_MASKED_SKIP)
+    return fail(h, SF_TM_CONFIG_ERROR, "masked_rows must be SF_TM_MASKED_*");
+  return SF_TM_OK;
+}
+
+int check_rows(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,
+               const int32_t* targets) {
+  if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
+  if (T < 0) return fail(h, SF_TM_CONFIG_ERROR, "T must be >= 0");
+  if (V <= 0 || V > (int64_t(1) << 31) - 1) return fail(h, SF_TM_CONFIG_ERROR, "V out of range");
+  if (ld < V) return fail(h, SF_TM_CONFIG_ERROR, "ld must be >= V");
+  if (T > 0 && (!logits || !targets))
+    return fail(h, SF_TM_CONFIG_ERROR, "logits and targets are required");
+  return SF_TM_OK;
+}
+
+void fill_loss(sftm::RowArgs& a, const sf_tm_loss_params* p) {
+  a.eps_lo = p->clip_eps_low;
+  a.eps_hi = p->clip_eps_high;
+  a.dual_c = p->dual_clip_c;
+  a.beta = p->kl_beta;
+  a.ent_coef = p->entropy_coef;
+  a.inv_tau = p->inv_temperature;
+  a.masked_skip = p->masked_rows == SF_TM_MASKED_SKIP ? 1 : 0;
+}
+
+int run_rows(sf_tm_t h, sftm::RowArgs& a, int mode, cudaStream_t s, const char* where) {
+  a.partials = h->partials;
+  a.ticket = h->ticket;
+  a.max_partial_blocks = h->max_partial_blocks;
+  sftm::LaunchInfo info;
+  const int e = sftm::launch_rows(a, mode, s, &h->err, &info);
+  h->launches += static_cast<uint64_t>(info.launches);
+  return check_cuda(h, e, where);
+}
+
+}  // namespace
+
+extern "C" {
+
+void sf_tm_default_loss_params(sf_tm_loss_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->clip_eps_low = 0.2f;
+  p->clip_eps_high = 0.28f;
+  p->dual_clip_c = 0.f;
+  p->kl_beta = 0.f;
+  p->entropy_coef = 0.f;
+  p->inv_temperature = 1.f;
+  p->norm_mode = SF_TM_NORM_TOKEN_MEAN;
+  p->inv_norm = 0.f;
+  p->masked_rows = SF_TM_MASKED_ZERO_FILL;
+}
+
+int sf_tm_abi_version(void) { return SF_TM_ABI_VERSION; }
+
+int sf_tm_create(int device, sf_tm_t* out) {
+  if (!out) return SF_TM_CONFIG_ERROR;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return SF_TM_INTERNAL;
+  if (device < 0 || device >= n) return SF_TM_CONFIG_ERROR;
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10 || minor != 0) return SF_TM_CONFIG_ERROR;  // built for sm_100a only
+  sf_tm_t h = new (std::nothrow) sf_tm_handle();
+  if (!h) return SF_TM_INTERNAL;
+  h->device = device;
+  if (use_device(h) != SF_TM_OK) {
+    delete h;
+    return SF_TM_INTERNAL;
+  }
+  h->max_partial_blocks = kMaxPartialBlocks;
+  if (cudaMalloc(&h->partials, sizeof(double) * 8 * kMaxPartialBlocks) != cudaSuccess ||
+      cudaMalloc(&h->ticket, sizeof(unsigned) * 2) != cudaSuccess ||
+      cudaMalloc(&h->tot, sizeof(int64_t) * 2) != cudaSuccess ||
+      cudaMalloc(&h->d_total, sizeof(int32_t)) != cudaSuccess ||
+      cudaMalloc(&h->d_metrics, sizeof(float) * SF_TM_NUM_METRICS) != cudaSuccess ||
+      cudaMemset(h->ticket, 0, sizeof(unsigned) * 2) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    sf_tm_destroy(h);
+    return SF_TM_INTERNAL;
+  }
+  h->ticket2 = h->ticket + 1;
+  *out = h;
+  return SF_TM_OK;
+}
+
+int sf_tm_destroy(sf_tm_t h) {
+  if (!h) return SF_TM_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != h->device) cudaSetDevice(h->device);
+  void* ptrs[] = {h->partials, h->ticket,  h->cnt,     h->tot,    h->d_targets, h->d_old,
+                  h->d_ref,    h->d_mask,  h->d_advtok, h->d_wtok, h->d_lens,    h->d_plens,
+                  h->d_rewards, h->d_gids, h->d_cu,    h->d_adv,  h->d_total,   h->d_metrics};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+  return SF_TM_OK;
+}
+
+const char* sf_tm_last_error(sf_tm_t h) { return h ? h->err.c_str() : "null handle"; }
+
+uint64_t sf_tm_launch_count(sf_tm_t h) { return h ? h->launches : 0; }
+
+int sf_tm_varlen_meta(sf_tm_t h, const int32_t* seq_lens, const int32_t* prompt_lens,
+                      const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,
+                      int32_t* seq_id, uint8_t* mask, int32_t* tok_group, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (B < 0 || T < 0) return fail(h, SF_TM_CONFIG_ERROR, "B and T must be >= 0");
+  if (!cu_seqlens || (B > 0 && !seq_lens))
+    return fail(h, SF_TM_CONFIG_ERROR, "seq_lens and cu_seqlens are required");
+  if (tok_group && !group_ids) return fail(h, SF_TM_CONFIG_ERROR, "tok_group needs group_ids");
+  int n = 0;
+  const int e = sftm::launch_varlen_meta(seq_lens, prompt_lens, group_ids, B, T, cu_seqlens,
+                                         seq_id, mask, tok_group, h->d_total,
+                                         static_cast<cudaStream_t>(stream), &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_varlen_meta");
+}
+
+int sf_tm_grpo_advantage(sf_tm_t h, const float* rewards, const int32_t* group_ids, int64_t B,
+                         float eps, int32_t std_mode, float* out_adv, int32_t* out_group_size,
+                         void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (B < 0) return fail(h, SF_TM_CONFIG_ERROR, "B must be >= 0");
+  if (std_mode < 0 || std_mode > 2) return fail(h, SF_TM_CONFIG_ERROR, "std_mode must be SF_TM_STD_*");
+  if (!(eps >= 0.f && std::isfinite(eps))) return fail(h, SF_TM_CONFIG_ERROR, "eps must be >= 0");
+  if (B == 0) return SF_TM_OK;
+  if (!rewards || !group_ids || !out_adv)
+    return fail(h, SF_TM_CONFIG_ERROR, "rewards, group_ids and out_adv are required");
+  int n = 0;
+  const int e = sftm::launch_grpo_advantage(rewards, group_ids, B, eps, std_mode, out_adv,
+                                            out_group_size, static_cast<cudaStream_t>(stream), &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_grpo_advantage");
+}
+
+int sf_tm_logprob_fwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                      int64_t ld, const int32_t* targets, float inv_temperature, float* out_logp,
+                      float* out_entropy, float* out_lse, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits, dtype, T, V, ld, targets)) return rc;
+  if (!(inv_temperature > 0.f && std::isfinite(inv_temperature)))
+    return fail(h, SF_TM_CONFIG_ERROR, "inv_temperature must be > 0");
+  if (T == 0) return SF_TM_OK;
+  sftm::RowArgs a;
+  a.logits = logits;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = V;
+  a.ld = ld;
+  a.targets = targets;
+  a.inv_tau = inv_temperature;
+  a.out_logp = out_logp;
+  a.out_entropy = out_entropy;
+  a.out_lse = out_lse;
+  return run_rows(h, a, sftm::kModeFwd, static_cast<cudaStream_t>(stream), "sf_tm_logprob_fwd");
+}
+
+int sf_tm_token_weights(sf_tm_t h, const int32_t* cu_seqlens, int64_t B, const float* adv_seq,
+                        const uint8_t* mask, int64_t T, int32_t norm_mode, float inv_norm,
+                        float* out_adv_tok, float* out_w_tok, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (B < 0 || T < 0) return fail(h, SF_TM_CONFIG_ERROR, "B and T must be >= 0");
+  if (norm_mode < 0 || norm_mode > 2) return fail(h, SF_TM_CONFIG_ERROR, "norm_mode must be SF_TM_NORM_*");
+  if (B == 0 || T == 0) return SF_TM_OK;
+  if (!cu_seqlens || !out_adv_tok || !out_w_tok)
+    return fail(h, SF_TM_CONFIG_ERROR, "cu_seqlens, out_adv_tok and out_w_tok are required");
+  if (int rc = ensure_cnt(h, B)) return rc;
+  int n = 0;
+  const int e = sftm::launch_token_weights(cu_seqlens, B, adv_seq, mask, T, norm_mode, inv_norm,
+                                           out_adv_tok, out_w_tok, h->cnt, h->ticket2, h->tot,
+                                           static_cast<cudaStream_t>(stream), &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_token_weights");
+}
+
+int sf_tm_pg_loss_fwd_bwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                          int64_t ld, const int32_t* targets, const float* old_logp,
+                          const float* ref_logp, const float* adv_tok, const float* w_tok,
+                          const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                          float* out_metrics, float* out_logp, float* out_entropy, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits, dtype, T, V, ld, targets)) return rc;
+  if (int rc = check_loss_params(h, params)) return rc;
+  if (!out_metrics) return fail(h, SF_TM_CONFIG_ERROR, "out_metrics is required");
+  if (ld_d < V) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= V");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (T == 0) {
+    return check_cuda(h, cudaMemsetAsync(out_metrics, 0, sizeof(float) * SF_TM_NUM_METRICS, s),
+                      "sf_tm_pg_loss_fwd_bwd");
+  }
+  if (!old_logp || !ref_logp || !adv_tok || !w_tok || !dlogits)
+    return fail(h, SF_TM_CONFIG_ERROR,
+                "old_logp, ref_logp, adv_tok, w_tok and dlogits are required");
+  if (dlogits == logits && ld_d != ld)
+    return fail(h, SF_TM_CONFIG_ERROR, "in-place dlogits needs ld_d == ld");
+  sftm::RowArgs a;
+  a.logits = logits;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = V;
+  a.ld = ld;
+  a.targets = targets;
+  a.old_logp = old_logp;
+  a.ref_logp = ref_logp;
+  a.adv_tok = adv_tok;
+  a.w_tok = w_tok;
+  fill_loss(a, params);
+  a.dlogits = dlogits;
+  a.ld_d = ld_d;
+  a.out_metrics = out_metrics;
+  a.out_logp = out_logp;
+  a.out_entropy = out_entropy;
+  return run_rows(h, a, sftm::kModeFwdBwd, s, "sf_tm_pg_loss_fwd_bwd");
+}
+
+int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
+                       int64_t ld, const int32_t* h_targets, const float* h_old_logp,
+                       const float* h_ref_logp, const uint8_t* h_mask, const int32_t* h_seq_lens,
+                       const int32_t* h_prompt_lens, const float* h_rewards,
+                       const int32_t* h_group_ids, int64_t B, float adv_eps, int32_t std_mode,
+                       const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                       float* h_metrics, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits, dtype, T, V, ld, h_targets)) return rc;
+  if (int rc = check_loss_params(h, params)) return rc;
+  if (B <= 0) return fail(h, SF_TM_CONFIG_ERROR, "B must be > 0");
+  if (!h_seq_lens || !h_rewards || !h_metrics || !h_old_logp || !h_ref_logp || !dlogits)
+    return fail(h, SF_TM_CONFIG_ERROR, "missing required host buffer");
+  if (adv_eps >= 0.f && !h_group_ids)
+    return fail(h, SF_TM_CONFIG_ERROR, "group ids are required to compute advantages");
+  if (std_mode < 0 || std_mode > 2) return fail(h, SF_TM_CONFIG_ERROR, "std_mode must be SF_TM_STD_*");
+  int64_t tsum = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    if (h_seq_lens[b] < 0) return fail(h, SF_TM_CONFIG_ERROR, "negative sequence length");
+    tsum += h_seq_lens[b];
+  }
+  if (tsum != T) return fail(h, SF_TM_CONFIG_ERROR, "sum(seq_lens) != T");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // grow-once scratch
+  if (T > h->tcap) {
+    const int64_t c = T;
+    int rc = 0;
+    if ((rc = grow(h, &h->d_targets, c, "scratch")) || (rc = grow(h, &h->d_old, c, "scratch")) ||
+        (rc = grow(h, &h->d_ref, c, "scratch")) || (rc = grow(h, &h->d_mask, c, "scratch")) ||
+        (rc = grow(h, &h->d_advtok, c, "scratch")) || (rc = grow(h, &h->d_wtok, c, "scratch")))
+      return rc;
+    h->tcap = c;
+  }
+  if (B > h->bcap) {
+    const int64_t c = B;
+    int rc = 0;
+    if ((rc = grow(h, &h->d_lens, c, "scratch")) || (rc = grow(h, &h->d_plens, c, "scratch")) ||
+        (rc = grow(h, &h->d_rewards, c, "scratch")) || (rc = grow(h, &h->d_gids, c, "scratch")) ||
+        (rc = grow(h, &h->d_cu, c + 1, "scratch")) || (rc = grow(h, &h->d_adv, c, "scratch")))
+      return rc;
+    h->bcap = c;
+  }
+  if (int rc = ensure_cnt(h, B)) return rc;
+  auto h2d = [&](void* d, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  cudaError_t e = cudaSuccess;
+  if ((e = h2d(h->d_targets, h_targets, sizeof(int32_t) * T)) ||
+      (e = h2d(h->d_old, h_old_logp, sizeof(float) * T)) ||
+      (e = h2d(h->d_ref, h_ref_logp, sizeof(float) * T)) ||
+      (e = h2d(h->d_lens, h_seq_lens, sizeof(int32_t) * B)) ||
+      (e = h2d(h->d_rewards, h_rewards, sizeof(float) * B)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
+  if (h_group_ids && (e = h2d(h->d_gids, h_group_ids, sizeof(int32_t) * B)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
+  if (h_prompt_lens && (e = h2d(h->d_plens, h_prompt_lens, sizeof(int32_t) * B)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
+  if (h_mask && (e = h2d(h->d_mask, h_mask, sizeof(uint8_t) * T)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
+
+  int n = 0;
+  int rc = sftm::launch_varlen_meta(h->d_lens, h_prompt_lens ? h->d_plens : nullptr, nullptr, B, T,
+                                    h->d_cu, nullptr,
+                                    (!h_mask && h_prompt_lens) ? h->d_mask : nullptr, nullptr,
+                                    h->d_total, s, &n);
+  h->launches += n;
+  if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host varlen");
+  const uint8_t* mask = (h_mask || h_prompt_lens) ? h->d_mask : nullptr;
+  const float* adv = h->d_rewards;
+  if (adv_eps >= 0.f) {
+    n = 0;
+    rc = sftm::launch_grpo_advantage(h->d_rewards, h->d_gids, B, adv_eps, std_mode, h->d_adv,
+                                     nullptr, s, &n);
+    h->launches += n;
+    if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host advantage");
+    adv = h->d_adv;
+  }
+  n = 0;
+  rc = sftm::launch_token_weights(h->d_cu, B, adv, mask, T, params->norm_mode, params->inv_norm,
+                                  h->d_advtok, h->d_wtok, h->cnt, h->ticket2, h->tot, s, &n);
+  h->launches += n;
+  if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host token weights");
+  sftm::RowArgs a;
+  a.logits = logits;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = V;
+  a.ld = ld;
+  a.targets = h->d_targets;
+  a.old_logp = h->d_old;
+  a.ref_logp = h->d_ref;
+  a.adv_tok = h->d_advtok;
+  a.w_tok = h->d_wtok;
+  fill_loss(a, params);
+  a.dlogits = dlogits;
+  a.ld_d = ld_d;
+  a.out_metrics = h->d_metrics;
+  if (int r2 = run_rows(h, a, sftm::kModeFwdBwd, s, "sf_tm_pg_step_host loss")) return r2;
+  e = cudaMemcpyAsync(h_metrics, h->d_metrics, sizeof(float) * SF_TM_NUM_METRICS,
+                      cudaMemcpyDeviceToHost, s);
+  return check_cuda(h, e, "sf_tm_pg_step_host D2H");
+}
+
+int sf_tm_r3_gate_fwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64_t L, int64_t T,
+                      int64_t E, int64_t k, const void* rec_idx, int32_t idx_dtype, int32_t renorm,
+                      float* out_w, int32_t* out_idx, uint32_t* out_mismatch, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
+  if (idx_dtype != SF_TM_IDX_I32 && idx_dtype != SF_TM_IDX_U8)
+    return fail(h, SF_TM_CONFIG_ERROR, "idx_dtype must be SF_TM_IDX_*");
+  if (L < 0 || T < 0) return fail(h, SF_TM_CONFIG_ERROR, "L and T must be >= 0");
+  if (E < 1 || E > 512) return fail(h, SF_TM_CONFIG_ERROR, "E must be in [1, 512]");
+  if (k < 1 || k > 32 || k > E) return fail(h, SF_TM_CONFIG_ERROR, "k must be in [1, min(32, E)]");
+  if (idx_dtype == SF_TM_IDX_U8 && E > 256)
+    return fail(h, SF_TM_CONFIG_ERROR, "u8 indices need E <= 256");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (out_mismatch) {
+    cudaError_t e = cudaMemsetAsync(out_mismatch, 0, sizeof(uint32_t) * (L + 1), s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sf_tm_r3_gate_fwd");
+  }
+  if (L * T == 0) return SF_TM_OK;
+  if (!router_logits || !rec_idx || !out_w)
+    return fail(h, SF_TM_CONFIG_ERROR, "router_logits, rec_idx and out_w are required");
+  int n = 0;
+  const int e = sftm::launch_r3_fwd(router_logits, dtype, L, T, E, k, rec_idx, idx_dtype, renorm,
+                                    out_w, out_idx, out_mismatch, s, &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_r3_gate_fwd");
+}
+
+int sf_tm_r3_gate_bwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64_t L, int64_t T,
+                      int64_t E, int64_t k, const void* rec_idx, int32_t idx_dtype, int32_t renorm,
+                      const float* w, const float* dw, void* dlogits, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
+  if (idx_dtype != SF_TM_IDX_I32 && idx_dtype != SF_TM_IDX_U8)
+    return fail(h, SF_TM_CONFIG_ERROR, "idx_dtype must be SF_TM_IDX_*");
+  if (L < 0 || T < 0) return fail(h, SF_TM_CONFIG_ERROR, "L and T must be >= 0");
+  if (E < 1 || E > 512) return fail(h, SF_TM_CONFIG_ERROR, "E must be in [1, 512]");
+  if (k < 1 || k > 32 || k > E) return fail(h, SF_TM_CONFIG_ERROR, "k must be in [1, min(32, E)]");
+  if (L * T == 0) return SF_TM_OK;
+  if (!rec_idx || !w || !dw || !dlogits || (!renorm && !router_logits))
+    return fail(h, SF_TM_CONFIG_ERROR, "missing required pointer");
+  int n = 0;
+  const int e = sftm::launch_r3_bwd(router_logits, dtype, L, T, E, k, rec_idx, idx_dtype, renorm,
+                                    w, dw, dlogits, static_cast<cudaStream_t>(stream), &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_r3_gate_bwd");
+}
+
+int sf_tm_vp_partial_stats(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T,
+                           int64_t Vp, int64_t ld, int64_t vocab_start, const int32_t* targets,
+                           float inv_temperature, float* out_stats, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits_shard, dtype, T, Vp, ld, targets)) return rc;
+  if (!(inv_temperature > 0.f && std::isfinite(inv_temperature)))
+    return fail(h, SF_TM_CONFIG_ERROR, "inv_temperature must be > 0");
+  if (vocab_start < 0) return fail(h, SF_TM_CONFIG_ERROR, "vocab_start must be >= 0");
+  if (T == 0) return SF_TM_OK;
+  if (!out_stats) return fail(h, SF_TM_CONFIG_ERROR, "out_stats is required");
+  sftm::RowArgs a;
+  a.logits = logits_shard;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = Vp;
+  a.ld = ld;
+  a.vocab_start = vocab_start;
+  a.targets = targets;
+  a.inv_tau = inv_temperature;
+  a.out_stats = out_stats;
+  return run_rows(h, a, sftm::kModeVpStats, static_cast<cudaStream_t>(stream),
+                  "sf_tm_vp_partial_stats");
+}
+
+int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T,
+                          int64_t Vp, int64_t ld, int64_t vocab_start, const float* gathered_stats,
+                          int32_t P, const int32_t* targets, const float* old_logp,
+                          const float* ref_logp, const float* adv_tok, const float* w_tok,
+                          const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
+                          float* out_metrics, float* out_logp, float* out_entropy, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits_shard, dtype, T, Vp, ld, targets)) return rc;
+  if (int rc = check_loss_params(h, params)) return rc;
+  if (P < 1) return fail(h, SF_TM_CONFIG_ERROR, "P must be >= 1");
+  if (vocab_start < 0) return fail(h, SF_TM_CONFIG_ERROR, "vocab_start must be >= 0");
+  if (!out_metrics) return fail(h, SF_TM_CONFIG_ERROR, "out_metrics is required");
+  if (ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= Vp");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (T == 0) {
+    return check_cuda(h, cudaMemsetAsync(out_metrics, 0, sizeof(float) * SF_TM_NUM_METRICS, s),
+                      "sf_tm_vp_loss_fwd_bwd");
+  }
+  if (!gathered_stats || !old_logp || !ref_logp || !adv_tok || !w_tok || !dlogits)
+    return fail(h, SF_TM_CONFIG_ERROR, "missing required pointer");
+  sftm::RowArgs a;
+  a.logits = logits_shard;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = Vp;
+  a.ld = ld;
+  a.vocab_start = vocab_start;
+  a.targets = targets;
+  a.gathered = gathered_stats;
+  a.P = P;
+  a.old_logp = old_logp;
+  a.ref_logp = ref_logp;
+  a.adv_tok = adv_tok;
+  a.w_tok = w_tok;
+  fill_loss(a, params);
+  a.dlogits = dlogits;
+  a.ld_d = ld_d;
+  a.out_metrics = out_metrics;
+  a.out_logp = out_logp;
+  a.out_entropy = out_entropy;
+  return run_rows(h, a, sftm::kModeVpBwd, s, "sf_tm_vp_loss_fwd_bwd");
+}
+
+int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,
+                       uint64_t seed, float sigma, const int32_t* peak_id, float peak_lo,
+                       float peak_hi, float outlier_frac, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
+  if (T < 0 || V <= 0 || ld < V) return fail(h, SF_TM_CONFIG_ERROR, "bad shape");
+  if (!(outlier_frac >= 0.f && outlier_frac <= 1.f))
+    return fail(h, SF_TM_CONFIG_ERROR, "outlier_frac must be in [0, 1]");
+  if (T == 0) return SF_TM_OK;
+  if (!logits) return fail(h, SF_TM_CONFIG_ERROR, "logits is NULL");
+  int n = 0;
+  const int e = sftm::launch_synth_logits(logits, dtype, T, V, ld, seed, sigma, peak_id, peak_lo,
+                                          peak_hi, outlier_frac, static_cast<cudaStream_t>(stream),
+                                          &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_synth_logits");
+}
+
+// Test hook (not in the public header): route row kernels to the generic path.
+int sf_tm_debug_force_generic(int on) {
+  sftm::set_force_generic(on != 0);
+  return SF_TM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// SPDX-License-Identifier: Apache-2.0
+// Internal interfaces between the C-ABI layer (tm_api.cu) and the kernel
+// translation units. Nothing here crosses the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace sftm {
+
+enum RowMode : int {
+  kModeFwd = 0,      // a1: logp / entropy / lse, one streaming pass
+  kModeFwdBwd = 1,   // a1+a4+a2: fused loss fwd+bwd, row resident in (cluster) smem
+  kModeVpStats = 2,  // a7 pass 1: partial stats of a vocab shard
+  kModeVpBwd = 3,    // a7 pass 2: combine gathered stats, loss, shard dlogits
+};
+
+struct RowArgs {
+  const void* logits = nullptr;
+  int dtype = 0;  // SF_TM_F32 / SF_TM_BF16
+  int64_t T = 0, V = 0, ld = 0;
+  int64_t vocab_start = 0;
+  const int32_t* targets = nullptr;
+  float inv_tau = 1.f;
+  // loss inputs
+  const float* old_logp = nullptr;
+  const float* ref_logp = nullptr;
+  const float* adv_tok = nullptr;
+  const float* w_tok = nullptr;
+  float eps_lo = 0.2f, eps_hi = 0.28f, dual_c = 0.f, beta = 0.f, ent_coef = 0.f;
+  int masked_skip = 0;
+  void* dlogits = nullptr;
+  int64_t ld_d = 0;
+  // outputs
+  float* out_logp = nullptr;
+  float* out_entropy = nullptr;
+  float* out_lse = nullptr;
+  float* out_stats = nullptr;  // VpStats: [T,4]
+  const float* gathered = nullptr;  // VpBwd: [P,T,4]
+  int P = 1;
+  float* out_metrics = nullptr;
+  // workspace (owned by the handle)
+  double* partials = nullptr;  // [max_blocks * 8]
+  unsigned* ticket = nullptr;
+  int max_partial_blocks = 0;
+};
+
+struct LaunchInfo {
+  int kernel = 0;  // 0 = ring (TMA) kernel, 1 = generic two-pass kernel
+  int cluster = 1;
+  int grid = 0;
+  int launches = 0;
+};
+
+// Launches the row kernel for `mode`. Returns 0 or a cudaError_t value; on a
+// config problem returns -1 with *err set.
+int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, LaunchInfo* info);
+
+// Forces the generic (non-TMA) kernel; used by tests to cover both paths.
+void set_force_generic(bool on);
+
+int launch_varlen_meta(const int32_t* seq_lens, const int32_t* prompt_lens,
+                       const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,
+                       int32_t* seq_id, uint8_t* mask, int32_t* tok_group, int32_t* d_total,
+                       cudaStream_t s, int* launches);
+
+int launch_grpo_advantage(const float* rewards, const int32_t* group_ids, int64_t B, float eps,
+                          int std_mode, float* out_adv, int32_t* out_group_size, cudaStream_t s,
+                          int* launches);
+
+int launch_token_weights(const int32_t* cu_seqlens, int64_t B, const float* adv_seq,
+                         const uint8_t* mask, int64_t T, int norm_mode, float inv_norm,
+                         float* out_adv_tok, float* out_w_tok, int32_t* scratch_cnt,
+                         unsigned* scratch_ticket, int64_t* scratch_tot, cudaStream_t s,
+                         int* launches);
+
+int launch_r3_fwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
+                  const void* rec_idx, int idx_dtype, int renorm, float* out_w, int32_t* out_idx,
+                  uint32_t* out_mismatch, cudaStream_t s, int* launches);
+
+int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
+                  const void* rec_idx, int idx_dtype, int renorm, const float* w, const float* dw,
+                  void* dlogits, cudaStream_t s, int* launches);
+
+int launch_synth_logits(void* logits, int dtype, int64_t T, int64_t V, int64_t ld, uint64_t seed,
+                        float sigma, const int32_t* peak_id, float peak_lo, float peak_hi,
+                        float outlier_frac, cudaStream_t s, int* launches);
+
+}  // namespace sftm

@@ -1,0 +1,294 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// a5: R3 Rollout Routing Replay gate (paper §5.5). The
+// trainer re-applies the top-k expert indices recorded at rollout time to its
+// own router logits instead of re-selecting them:
+//   renorm=1 (P8): w_j = softmax_j(z[e_j]) over the k recorded experts;
+//   renorm=0:      w_j = softmax(z)[e_j] over all E experts.
+// The replayed indices are passed through bit-exactly, and the trainer's own
+// top-k set (ties -> lowest expert index, P9) is compared with the recorded
+// set per token to count routing mismatches per layer.
+//
+// Layout: rows are (layer, token) pairs, layer-major [L*T, E]. One warp per
+// row; expert e lives in lane e%32, register e/32 (coalesced row loads).
+// Each warp owns a contiguous row range so mismatch counts are flushed with
+// one integer atomic per (warp, layer) — integer atomics keep the count exact.
+
+#include <cuda_runtime.h>
+
+#include "tm_device.cuh"
+#include "tm_internal.h"
+
+namespace sftm {
+
+template <typename T>
+__device__ __forceinline__ float r3_load(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float r3_load<float>(const float* p, int64_t i) {
+  return __ldg(p + i);
+}
+template <>
+__device__ __forceinline__ float r3_load<uint16_t>(const uint16_t* p, int64_t i) {
+  return bf16_to_f32(__ldg(reinterpret_cast<const unsigned short*>(p) + i));
+}
+__device__ __forceinline__ int32_t r3_idx(const void* p, int idx_dtype, int64_t i) {
+  if (idx_dtype == 1) return static_cast<int32_t>(__ldg(static_cast<const uint8_t*>(p) + i));
+  return __ldg(static_cast<const int32_t*>(p) + i);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, int NPL>
+__global__ void __launch_bounds__(256)
+    r3_fwd_kernel(const T* __restrict__ logits, int64_t L, int64_t Tn, int E, int k,
+                  const void* __restrict__ rec, int idx_dtype, int renorm, float* __restrict__ out_w,
+                  int32_t* __restrict__ out_idx, uint32_t* __restrict__ mismatch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t rows = L * Tn;
+  const int64_t per = (rows + nw - 1) / nw;
+  const int64_t r0 = gw * per;
+  int64_t r1 = r0 + per;
+  if (r1 > rows) r1 = rows;
+  int64_t cur_layer = -1;
+  uint32_t cur_cnt = 0;
+
+  for (int64_t row = r0; row < r1; ++row) {
+    const int64_t layer = row / Tn;
+    if (layer != cur_layer) {
+      if (cur_cnt && lane == 0 && mismatch) {
+        atomicAdd(mismatch + cur_layer, cur_cnt);
+        atomicAdd(mismatch + L, cur_cnt);
+      }
+      cur_layer = layer;
+      cur_cnt = 0;
+    }
+    float z[NPL];
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int e = i * 32 + lane;
+      z[i] = (e < E) ? r3_load(logits, row * E + e) : -INFINITY;
+    }
+    int32_t my_e = -1;
+    if (lane < k) my_e = r3_idx(rec, idx_dtype, row * k + lane);
+    // gather z at my recorded expert
+    float zr = -INFINITY;
+    {
+      const int src = my_e & 31, reg = my_e >> 5;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const float v = __shfl_sync(0xffffffffu, z[i], src);
+        if (reg == i) zr = v;
+      }
+      if (my_e < 0 || my_e >= E) zr = (lane < k) ? __int_as_float(0x7fc00000) : -INFINITY;
+    }
+    float wj;
+    if (renorm) {
+      const float mx = warp_max(lane < k ? zr : -INFINITY);
+      const float ez = (lane < k) ? expf(zr - mx) : 0.f;
+      const float sum = warp_sum(ez);
+      wj = ez / sum;
+    } else {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) mx = fmaxf(mx, z[i]);
+      mx = warp_max(mx);
+      float se = 0.f;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) se += expf(z[i] - mx);
+      se = warp_sum(se);
+      wj = expf(zr - mx) / se;
+    }
+    if (lane < k) {
+      out_w[row * k + lane] = wj;
+      if (out_idx) out_idx[row * k + lane] = my_e;
+    }
+    if (mismatch) {
+      // trainer top-k, ties -> lowest expert index (P9)
+      uint32_t taken = 0;
+      for (int r = 0; r < k; ++r) {
+        float bv = -INFINITY;
+        int be = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+          const int e = i * 32 + lane;
+          if (e < E && !((taken >> i) & 1u)) {
+            if (z[i] > bv || (z[i] == bv && e < be)) {
+              bv = z[i];
+              be = e;
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+          if (ov > bv || (ov == bv && oe < be)) {
+            bv = ov;
+            be = oe;
+          }
+        }
+        if (be != 0x7fffffff && (be & 31) == lane) taken |= 1u << (be >> 5);
+      }
+      uint32_t recm = 0;
+      for (int j = 0; j < k; ++j) {
+        const int e = __shfl_sync(0xffffffffu, my_e, j);
+        if (e >= 0 && e < E && (e & 31) == lane) recm |= 1u << (e >> 5);
+      }
+      if (__any_sync(0xffffffffu, recm != taken)) ++cur_cnt;
+    }
+  }
+  if (cur_cnt && lane == 0 && mismatch) {
+    atomicAdd(mismatch + cur_layer, cur_cnt);
+    atomicAdd(mismatch + L, cur_cnt);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void r3_store(T* p, int64_t i, float v);
+template <>
+__device__ __forceinline__ void r3_store<float>(float* p, int64_t i, float v) {
+  p[i] = v;
+}
+template <>
+__device__ __forceinline__ void r3_store<uint16_t>(uint16_t* p, int64_t i, float v) {
+  p[i] = f32_to_bf16(v);
+}
+
+template <typename T, int NPL>
+__global__ void __launch_bounds__(256)
+    r3_bwd_kernel(const T* __restrict__ logits, int64_t rows, int E, int k,
+                  const void* __restrict__ rec, int idx_dtype, int renorm,
+                  const float* __restrict__ w, const float* __restrict__ dw, T* __restrict__ dz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t row = gw; row < rows; row += nw) {
+    int32_t my_e = -1;
+    float wj = 0.f, dwj = 0.f;
+    if (lane < k) {
+      my_e = r3_idx(rec, idx_dtype, row * k + lane);
+      wj = w[row * k + lane];
+      dwj = dw[row * k + lane];
+    }
+    const float S = warp_sum(wj * dwj);
+    float out[NPL];
+    if (renorm) {
+      const float val = wj * (dwj - S);
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) out[i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int e = __shfl_sync(0xffffffffu, my_e, j);
+        const float v = __shfl_sync(0xffffffffu, val, j);
+        if (e >= 0 && e < E && (e & 31) == lane) {
+#pragma unroll
+          for (int i = 0; i < NPL; ++i)
+            if ((e >> 5) == i) out[i] += v;
+        }
+      }
+    } else {
+      float z[NPL], mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const int e = i * 32 + lane;
+        z[i] = (e < E) ? r3_load(logits, row * E + e) : -INFINITY;
+        mx = fmaxf(mx, z[i]);
+      }
+      mx = warp_max(mx);
+      float se = 0.f;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) se += expf(z[i] - mx);
+      se = warp_sum(se);
+      float D[NPL];
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) D[i] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int e = __shfl_sync(0xffffffffu, my_e, j);
+        const float v = __shfl_sync(0xffffffffu, dwj, j);
+        if (e >= 0 && e < E && (e & 31) == lane) {
+#pragma unroll
+          for (int i = 0; i < NPL; ++i)
+            if ((e >> 5) == i) D[i] += v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) out[i] = expf(z[i] - mx) / se * (D[i] - S);
+    }
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int e = i * 32 + lane;
+      if (e < E) r3_store(dz, row * E + e, out[i]);
+    }
+  }
+}
+
+namespace {
+int r3_grid(int64_t rows) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t g = (rows + 7) / 8;
+  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+}  // namespace
+
+#define SFTM_R3_NPL(E, X) \
+  ((E) <= 32 ? X(1) : (E) <= 64 ? X(2) : (E) <= 128 ? X(4) : (E) <= 256 ? X(8) : X(16))
+
+int launch_r3_fwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
+                  const void* rec_idx, int idx_dtype, int renorm, float* out_w, int32_t* out_idx,
+                  uint32_t* out_mismatch, cudaStream_t s, int* launches) {
+  const int grid = r3_grid(L * T);
+#define LAUNCH_F(NPL)                                                                           \
+  (dtype == 1 ? (r3_fwd_kernel<uint16_t, NPL><<<grid, 256, 0, s>>>(                             \
+                     static_cast<const uint16_t*>(logits), L, T, static_cast<int>(E),          \
+                     static_cast<int>(k), rec_idx, idx_dtype, renorm, out_w, out_idx,          \
+                     out_mismatch),                                                             \
+                 0)                                                                             \
+              : (r3_fwd_kernel<float, NPL><<<grid, 256, 0, s>>>(                                \
+                     static_cast<const float*>(logits), L, T, static_cast<int>(E),             \
+                     static_cast<int>(k), rec_idx, idx_dtype, renorm, out_w, out_idx,          \
+                     out_mismatch),                                                             \
+                 0))
+  (void)SFTM_R3_NPL(E, LAUNCH_F);
+#undef LAUNCH_F
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
+                  const void* rec_idx, int idx_dtype, int renorm, const float* w, const float* dw,
+                  void* dlogits, cudaStream_t s, int* launches) {
+  const int64_t rows = L * T;
+  const int grid = r3_grid(rows);
+#define LAUNCH_B(NPL)                                                                           \
+  (dtype == 1 ? (r3_bwd_kernel<uint16_t, NPL><<<grid, 256, 0, s>>>(                             \
+                     static_cast<const uint16_t*>(logits), rows, static_cast<int>(E),          \
+                     static_cast<int>(k), rec_idx, idx_dtype, renorm, w, dw,                   \
+                     static_cast<uint16_t*>(dlogits)),                                          \
+                 0)                                                                             \
+              : (r3_bwd_kernel<float, NPL><<<grid, 256, 0, s>>>(                                \
+                     static_cast<const float*>(logits), rows, static_cast<int>(E),             \
+                     static_cast<int>(k), rec_idx, idx_dtype, renorm, w, dw,                   \
+                     static_cast<float*>(dlogits)),                                             \
+                 0))
+  (void)SFTM_R3_NPL(E, LAUNCH_B);
+#undef LAUNCH_B
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace sftm

@@ -1,0 +1,57 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Comparison helpers with the tolerances of DESIGN.md §3 written out."""
+import numpy as np
+
+# logp / entropy / lse / loss vs the fp64 oracle: |d| <= ATOL + RTOL*|ref|
+ATOL = 1e-5
+RTOL = 1e-5
+
+
+def assert_close(got, ref, atol=ATOL, rtol=RTOL, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(got - ref)
+    lim = atol + rtol * np.abs(ref)
+    bad = ~(err <= lim)
+    if bad.any():
+        i = np.flatnonzero(bad.ravel())[:5]
+        raise AssertionError(f"{what}: {bad.sum()} / {bad.size} out of tolerance; e.g. idx {i} got "
+                             f"{got.ravel()[i]} ref {ref.ravel()[i]} (atol {atol}, rtol {rtol})")
+
+
+def bf16_ulp(v: np.ndarray) -> np.ndarray:
+    """Spacing of the bf16 grid at |v| (8 significant bits)."""
+    a = np.abs(v)
+    e = np.floor(np.log2(np.maximum(a, 1e-38)))
+    return np.exp2(e - 7)
+
+
+def assert_grad_close(got, ref, row_scale, dtype, what="dlogits", rows_ok=None):
+    """dlogits: bf16 -> within 1 bf16 ulp of the exact value (plus a row-scale
+    floor for cancellation at the target entry); f32 -> rel 1e-5.
+    row_scale[t] ~ |dL/dlogp_t| * inv_tau (+ entropy term scale)."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    floor = 4e-6 * np.asarray(row_scale, dtype=np.float64)[:, None] + 1e-30
+    if dtype == "bf16":
+        lim = bf16_ulp(ref) + floor
+    else:
+        lim = 1e-5 * np.abs(ref) + floor
+    bad = ~(np.abs(got - ref) <= lim)
+    if rows_ok is not None:
+        bad &= rows_ok[:, None]
+    if bad.any():
+        r, c = np.nonzero(bad)
+        raise AssertionError(f"{what}: {bad.sum()} entries out of tolerance in rows {np.unique(r)[:8]}; "
+                             f"e.g. ({r[0]},{c[0]}) got {got[r[0], c[0]]!r} ref {ref[r[0], c[0]]!r}")
+
+
+def near_clip_rows(logp_ref, old, adv, eps_lo, eps_hi, dual_c=0.0, tol=1e-5):
+    """Rows whose ratio sits within tol of a clip decision boundary, where an
+    fp32 kernel and the fp64 oracle may legitimately take different branches."""
+    r = np.exp(np.asarray(logp_ref) - np.asarray(old, dtype=np.float64))
+    a = np.asarray(adv, dtype=np.float64)
+    near = (np.abs(r - (1 + eps_hi)) < tol * (1 + eps_hi)) | (np.abs(r - (1 - eps_lo)) < tol)
+    if dual_c > 1:
+        near |= (a < 0) & (np.abs(r - dual_c) < tol * dual_c)
+    return near

@@ -1,0 +1,402 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity: every C-ABI entry point vs the fp64 oracle on the same seeded
+inputs. Bit-exact for integer/index work (cu_seqlens, seq ids,
+masks, group ids/sizes, replayed expert indices, mismatch counts); stated
+tolerances (tests/_cmp.py) for floating point."""
+import numpy as np
+import pytest
+
+from tests._cmp import assert_close, assert_grad_close, near_clip_rows
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tm():
+    from paper_2604_11554_b200 import train_math
+
+    train_math.handle(0)
+    return train_math
+
+
+def to_dev_logits(prob):
+    x = prob["logits"]
+    if x.dtype == np.uint16:
+        return torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()
+    return torch.from_numpy(x).cuda()
+
+
+def grad_to_np(dl):
+    if dl.dtype == torch.bfloat16:
+        from oracle.oracle import bf16_bits_to_f32
+
+        return bf16_bits_to_f32(dl.view(torch.int16).cpu().numpy().view(np.uint16)).astype(np.float64)
+    return dl.cpu().numpy().astype(np.float64)
+
+
+def i32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def f32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def gpu_pipeline(tm, prob, norm_mode=0, adv_eps=1e-6, std_mode=0):
+    lens = i32(prob["lens"])
+    cu, sid, mask, _ = tm.varlen_meta(lens, i32(prob["plens"]), T=prob["T"])
+    adv = tm.grpo_advantage(f32(prob["rewards"]), i32(prob["gids"]), adv_eps, std_mode)
+    adv_tok, w_tok = tm.token_weights(cu, adv, mask, prob["T"], norm_mode)
+    return cu, sid, mask, adv, adv_tok, w_tok
+
+
+def check_loss_case(tm, orc, prob, pkw=None, generic=False, in_place=False, masked_skip=False, norm_mode=0):
+    pkw = dict(pkw or {})
+    from paper_2604_11554_b200 import _lib
+
+    params = _lib.default_loss_params(**pkw)
+    params.norm_mode = norm_mode
+    if masked_skip:
+        params.masked_rows = _lib.MASKED_SKIP
+    logits = to_dev_logits(prob)
+    cu, sid, mask, adv, adv_tok, w_tok = gpu_pipeline(tm, prob, norm_mode)
+    tm.set_force_generic(generic)
+    try:
+        sentinel = None
+        if masked_skip:
+            dl = torch.full_like(logits, 7.0)
+            sentinel = 7.0
+        else:
+            dl = None
+        met, dl, logp, ent = tm.pg_loss_fwd_bwd(logits, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]),
+                                                adv_tok, w_tok, params, dlogits=dl, in_place=in_place, want_logp=True)
+        torch.cuda.synchronize()
+    finally:
+        tm.set_force_generic(False)
+    w = w_tok.cpu().numpy()
+    a = adv_tok.cpu().numpy()
+    op = orc.params(params.clip_eps_low, params.clip_eps_high, params.dual_clip_c, params.kl_beta,
+                    params.entropy_coef, params.inv_temperature)
+    om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, op,
+                                                 masked_skip=masked_skip)
+    act = w != 0
+    gl = logp.cpu().numpy()
+    ge = ent.cpu().numpy()
+    assert_close(gl[act], olp[act], what="logp")
+    assert_close(ge[act], oent[act], what="entropy")
+    gm = met.cpu().numpy()
+    near = near_clip_rows(olp, prob["old"], a, params.clip_eps_low, params.clip_eps_high, params.dual_clip_c)
+    near &= act
+    scale = (np.abs(og) + np.abs(w) * abs(params.entropy_coef) * 60.0) * params.inv_temperature
+    gdl = grad_to_np(dl)
+    if masked_skip:
+        assert np.all(gdl[~act] == sentinel)
+        rows = act & ~near
+    else:
+        rows = ~near
+    assert_grad_close(gdl, odl, scale, prob["dtype"], rows_ok=rows)
+    if not near.any():
+        tol = 1e-5 * (np.abs(w) * (np.abs(a) * 2 + 1)).sum() + 1e-6
+        for i, name in enumerate(["loss", "pg", "kl", "entropy", "clipfrac", "ratio", "n_active", "ppo_kl"]):
+            if name == "n_active":
+                assert gm[i] == om[i]
+            else:
+                t = tol * (30 if name in ("kl", "entropy") else 1)
+                assert abs(gm[i] - om[i]) <= t, (name, gm[i], om[i])
+    return gm, gdl
+
+
+# ---------------------------------------------------------------------------- a6 / a3 / a4 prologue
+def test_varlen_meta_bit_exact(tm, orc):
+    rng = np.random.default_rng(11)
+    lens = rng.integers(0, 300, size=257).astype(np.int32)
+    lens[[0, 5, 100]] = 0
+    plens = rng.integers(0, 400, size=257).astype(np.int32)
+    gids = rng.integers(-5, 50, size=257).astype(np.int32)
+    cu, sid, mask, tg = tm.varlen_meta(i32(lens), i32(plens), i32(gids), T=int(lens.sum()))
+    ocu, osid, omask, otg = orc.varlen_meta(lens, plens, gids)
+    for g, o in ((cu, ocu), (sid, osid), (mask, omask), (tg, otg)):
+        g = g.cpu().numpy()
+        assert orc.digest(g) == orc.digest(o)
+
+
+def test_varlen_meta_large_b(tm, orc):
+    lens = (np.arange(5000) % 7).astype(np.int32)
+    cu, _, _, _ = tm.varlen_meta(i32(lens), T=int(lens.sum()), want=("cu",))
+    assert orc.digest(cu.cpu().numpy()) == orc.digest(orc.varlen_meta(lens)[0])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_grpo_advantage_golden(tm, orc, mode):
+    import os
+
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_grpo.npz"))
+    adv, gs = tm.grpo_advantage(f32(d["rewards"]), i32(d["gids"]), 1e-6, mode, want_group_size=True)
+    oadv, ogs = orc.grpo_advantage(d["rewards"], d["gids"], 1e-6, mode)
+    assert np.array_equal(gs.cpu().numpy(), ogs)
+    got = adv.cpu().numpy()
+    assert_close(got, oadv, atol=1e-6, rtol=1e-6, what="advantage")
+    eq = oadv == 0.0
+    assert np.all(got[eq] == 0.0)  # P3: zero-variance groups are exactly 0
+
+
+def test_grpo_advantage_large_noncontiguous(tm, orc):
+    rng = np.random.default_rng(12)
+    B = 4096
+    gids = rng.permutation(np.repeat(np.arange(256), 16)).astype(np.int32)
+    r = rng.random(B).astype(np.float32)
+    adv, gs = tm.grpo_advantage(f32(r), i32(gids), 1e-6, 0, want_group_size=True)
+    oadv, ogs = orc.grpo_advantage(r, gids)
+    assert np.array_equal(gs.cpu().numpy(), ogs)
+    assert_close(adv.cpu().numpy(), oadv, atol=1e-6, rtol=1e-6, what="advantage")
+
+
+@pytest.mark.parametrize("norm_mode", [0, 1, 2])
+def test_token_weights(tm, orc, norm_mode):
+    rng = np.random.default_rng(13)
+    lens = rng.integers(0, 50, size=40).astype(np.int32)
+    T = int(lens.sum())
+    cu = orc.varlen_meta(lens)[0]
+    mask = (rng.random(T) < 0.7).astype(np.uint8)
+    adv = rng.normal(size=40).astype(np.float32)
+    at, wt = tm.token_weights(i32(cu), f32(adv), torch.from_numpy(mask).cuda(), T, norm_mode, 0.125)
+    oat, owt = orc.token_weights(cu, adv, mask, T, norm_mode, 0.125)
+    assert np.array_equal(at.cpu().numpy(), oat.astype(np.float32))
+    assert_close(wt.cpu().numpy(), owt, atol=0, rtol=1e-7, what="w_tok")
+
+
+# ---------------------------------------------------------------------------- a1
+@pytest.mark.parametrize("dtype,V,T,generic", [("bf16", 151936, 40, False), ("bf16", 151936, 40, True),
+                                               ("f32", 32000, 64, False), ("bf16", 1001, 33, False),
+                                               ("f32", 151936, 9, False), ("bf16", 8, 5, False)])
+def test_logprob_fwd(tm, orc, dtype, V, T, generic):
+    lens = [T]
+    prob = orc.synth_problem(100 + V % 97, lens, V, dtype)
+    logits = to_dev_logits(prob)
+    tm.set_force_generic(generic)
+    try:
+        logp, ent, lse = tm.logprob_fwd(logits, i32(prob["targets"]))
+        torch.cuda.synchronize()
+    finally:
+        tm.set_force_generic(False)
+    olp, oent, olse = orc.logprob_fwd(prob["logits"], prob["targets"])
+    assert_close(logp.cpu().numpy(), olp, what="logp")
+    assert_close(ent.cpu().numpy(), oent, what="entropy")
+    assert_close(lse.cpu().numpy(), olse, what="lse")
+
+
+def test_logprob_fwd_temperature_and_strided_rows(tm, orc):
+    prob = orc.synth_problem(5, [24], 32000, "bf16")
+    big = torch.zeros(24, 32064, dtype=torch.bfloat16, device="cuda")
+    big[:, :32000] = to_dev_logits(prob)
+    view = big[:, :32000]
+    logp, ent, lse = tm.logprob_fwd(view, i32(prob["targets"]), inv_temperature=1 / 0.6)
+    olp, oent, olse = orc.logprob_fwd(prob["logits"], prob["targets"], 1 / 0.6)
+    assert_close(logp.cpu().numpy(), olp, what="logp")
+    assert_close(ent.cpu().numpy(), oent, what="entropy")
+
+
+# ---------------------------------------------------------------------------- a1+a4+a2 fused
+LOSS_CASES = [
+    # id, dtype, V, lens, params, kwargs
+    ("qwen_bf16_c2", "bf16", 151936, [17, 9, 30, 8], {}, {}),
+    ("qwen_bf16_generic", "bf16", 151936, [17, 9, 30, 8], {}, {"generic": True}),
+    ("cfg1_f32", "f32", 32000, [40, 3, 21], {}, {}),
+    ("kl_ent_tau_bf16", "bf16", 32000, [20, 20], {"kl_beta": 0.05, "entropy_coef": 0.01, "inv_temperature": 1 / 0.7}, {}),
+    ("dualclip_f32", "f32", 4096, [30, 30], {"dual_clip_c": 3.0, "clip_eps_low": 0.1, "clip_eps_high": 0.15}, {}),
+    ("inplace_bf16", "bf16", 151936, [12, 12], {}, {"in_place": True}),
+    ("masked_skip_bf16", "bf16", 32000, [25, 25], {}, {"masked_skip": True}),
+    ("seq_mean_bf16", "bf16", 32000, [25, 5, 25], {}, {"norm_mode": 1}),
+    ("f32_wide_c4", "f32", 151936, [6, 4], {}, {}),
+    ("bf16_c8_262k", "bf16", 262144, [5], {}, {}),
+    ("bf16_odd_vocab_generic", "bf16", 50257, [10, 7], {}, {}),
+    ("bf16_tiny_vocab", "bf16", 16, [9, 9], {"kl_beta": 0.1}, {}),
+]
+
+
+@pytest.mark.parametrize("case", LOSS_CASES, ids=[c[0] for c in LOSS_CASES])
+def test_pg_loss_fwd_bwd(tm, orc, case):
+    _, dtype, V, lens, pkw, kw = case
+    prob = orc.synth_problem(abs(hash(case[0])) % 1000, lens, V, dtype, prompt_max=8)
+    check_loss_case(tm, orc, prob, pkw, **kw)
+
+
+def test_pg_loss_deterministic(tm, orc):
+    prob = orc.synth_problem(77, [64, 64], 151936, "bf16")
+    m1, d1 = check_loss_case(tm, orc, prob)
+    m2, d2 = check_loss_case(tm, orc, prob)
+    assert np.array_equal(m1, m2)
+    assert np.array_equal(d1, d2)
+
+
+def test_pg_loss_all_masked_and_empty(tm, orc):
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(3, [6], 4096, "bf16")
+    logits = to_dev_logits(prob)
+    z = torch.zeros(6, device="cuda")
+    met, dl, _, _ = tm.pg_loss_fwd_bwd(logits, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]), z, z)
+    assert torch.all(met == 0) and torch.all(dl == 0)
+    e = torch.empty(0, 4096, dtype=torch.bfloat16, device="cuda")
+    ei = torch.empty(0, dtype=torch.int32, device="cuda")
+    ef = torch.empty(0, device="cuda")
+    met, _, _, _ = tm.pg_loss_fwd_bwd(e, ei, ef, ef, ef, ef)
+    assert torch.all(met.cpu() == 0)
+    with pytest.raises(_lib.TrainMathError) as ex:
+        tm.pg_loss_fwd_bwd(logits, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]), z, z,
+                           _lib.default_loss_params(inv_temperature=0.0))
+    assert ex.value.code == _lib.CONFIG_ERROR
+
+
+def test_pg_step_host_matches_oracle_pipeline(tm, orc):
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(21, [50, 40, 33, 61, 12, 70, 8, 30], 32000, "bf16", prompt_max=20, G=4)
+    logits = to_dev_logits(prob)
+    pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()
+    hm, dl = tm.pg_step_host(logits, pin(prob["targets"], np.int32), pin(prob["old"], np.float32),
+                             pin(prob["ref"], np.float32), pin(prob["lens"], np.int32), pin(prob["rewards"], np.float32),
+                             pin(prob["gids"], np.int32), h_prompt_lens=pin(prob["plens"], np.int32))
+    torch.cuda.synchronize()
+    cu, _, mask, _ = orc.varlen_meta(prob["lens"], prob["plens"])
+    adv, _ = orc.grpo_advantage(prob["rewards"], prob["gids"])
+    at, wt = orc.token_weights(cu, adv.astype(np.float32), mask, prob["T"])
+    om, odl, olp, _, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"],
+                                              at.astype(np.float32), wt.astype(np.float32))
+    near = near_clip_rows(olp, prob["old"], at, 0.2, 0.28) & (wt != 0)
+    assert_grad_close(grad_to_np(dl), odl, np.abs(og), "bf16", rows_ok=~near)
+    gm = hm.numpy()
+    assert gm[_lib.NUM_METRICS - 2] == om[6]
+    if not near.any():
+        assert_close(gm[:6], om[:6], atol=2e-5, rtol=1e-4, what="metrics")
+
+
+# ---------------------------------------------------------------------------- a7 vocab parallel (1-GPU emulation)
+@pytest.mark.parametrize("P", [2, 4])
+def test_vocab_parallel_matches_fused(tm, orc, P):
+    prob = orc.synth_problem(31, [20, 12], 151936, "bf16", prompt_max=4)
+    logits = to_dev_logits(prob)
+    cu, sid, mask, adv, adv_tok, w_tok = gpu_pipeline(tm, prob)
+    tg = i32(prob["targets"])
+    old, ref = f32(prob["old"]), f32(prob["ref"])
+    met_f, dl_f, lp_f, _ = tm.pg_loss_fwd_bwd(logits, tg, old, ref, adv_tok, w_tok, want_logp=True)
+    V = prob["V"]
+    b = np.linspace(0, V, P + 1).astype(int) // 8 * 8
+    b[-1] = V
+    shards = [logits[:, b[i]:b[i + 1]].contiguous() for i in range(P)]
+    stats = torch.stack([tm.vp_partial_stats(s, tg, int(b[i])) for i, s in enumerate(shards)])
+    # partial stats vs oracle
+    for i, s in enumerate(shards):
+        ost = orc.vp_partial_stats(prob["logits"][:, b[i]:b[i + 1]], prob["targets"], int(b[i]))
+        g = stats[i].cpu().numpy()
+        assert_close(g[:, 0], ost[:, 0], what="m")
+        assert_close(g[:, 1], ost[:, 1], atol=0, rtol=2e-6, what="s")
+        assert np.array_equal(np.isnan(g[:, 3]), np.isnan(ost[:, 3]))
+    dls, mets = [], []
+    for i, s in enumerate(shards):
+        m, d, lp, _ = tm.vp_loss_fwd_bwd(s, int(b[i]), stats, tg, old, ref, adv_tok, w_tok, want_logp=True)
+        dls.append(d)
+        mets.append(m)
+        assert_close(lp.cpu().numpy(), lp_f.cpu().numpy(), atol=2e-6, rtol=2e-6, what="vp logp")
+    dl = torch.cat(dls, 1)
+    a = adv_tok.cpu().numpy()
+    w = w_tok.cpu().numpy()
+    om, odl, olp, _, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w)
+    near = near_clip_rows(olp, prob["old"], a, 0.2, 0.28)
+    assert_grad_close(grad_to_np(dl), odl, np.abs(og), "bf16", rows_ok=~near)
+    for m in mets[1:]:
+        assert torch.equal(m, mets[0])  # identical on every rank
+    assert_close(mets[0].cpu().numpy()[:6], met_f.cpu().numpy()[:6], atol=2e-6, rtol=2e-5, what="vp metrics")
+
+
+# ---------------------------------------------------------------------------- a5 R3
+@pytest.mark.parametrize("dtype,idx_dtype,renorm", [("f32", "i32", True), ("bf16", "u8", True), ("f32", "i32", False),
+                                                    ("bf16", "i32", False)])
+def test_r3_gate(tm, orc, dtype, idx_dtype, renorm):
+    rng = np.random.default_rng(41)
+    L, T, E, k = 4, 300, 128, 8
+    z = (rng.normal(size=(L, T, E)) * 2).astype(np.float32)
+    if dtype == "bf16":
+        zb = orc.f32_to_bf16_bits(z).reshape(L, T, E)
+        z = orc.bf16_bits_to_f32(zb).reshape(L, T, E)
+        zin, zt = zb, torch.from_numpy(zb.view(np.int16)).view(torch.bfloat16).cuda()
+    else:
+        zin, zt = z, torch.from_numpy(z).cuda()
+    z[1, :3] = 0.0  # fully tied rows (P9)
+    if dtype == "bf16":
+        zin[1, :3] = 0
+        zt[1, :3] = 0
+    else:
+        zt[1, :3] = 0
+    order = np.lexsort((np.broadcast_to(np.arange(E), z.shape), -z), axis=-1)
+    rec = order[..., :k].copy()
+    flip = rng.random((L, T)) < 0.05
+    for l, t in zip(*np.nonzero(flip)):
+        others = np.setdiff1d(np.arange(E), rec[l, t])
+        rec[l, t, rng.integers(0, k)] = rng.choice(others)
+    rec = rec.astype(np.uint8 if idx_dtype == "u8" else np.int32)
+    rt = torch.from_numpy(rec).cuda()
+    w, idx, mm = tm.r3_gate_fwd(zt, rt, renorm=renorm)
+    ow, oidx, omm = orc.r3_gate_fwd(zin, rec, renorm=renorm)
+    assert orc.digest(idx.cpu().numpy()) == orc.digest(oidx)  # replayed indices bit-exact
+    assert np.array_equal(mm.cpu().numpy().astype(np.uint32), omm)
+    assert omm[L] == flip.sum()
+    assert_close(w.cpu().numpy(), ow, atol=1e-6, rtol=1e-5, what="r3 w")
+    dw = rng.normal(size=(L, T, k)).astype(np.float32)
+    wg = w.cpu().numpy()
+    dz = tm.r3_gate_bwd(zt, rt, w, torch.from_numpy(dw).cuda(), renorm=renorm)
+    odz = orc.r3_gate_bwd(zin, rec, wg, dw, renorm=renorm)
+    g = grad_to_np(dz.reshape(L * T, E)).reshape(L, T, E)
+    if dtype == "bf16":
+        from tests._cmp import bf16_ulp
+
+        assert np.all(np.abs(g - odz) <= bf16_ulp(odz) + 1e-6)
+    else:
+        assert_close(g, odz, atol=1e-6, rtol=1e-5, what="r3 dz")
+
+
+# ---------------------------------------------------------------------------- full-size properties
+def test_full_vocab_large_batch_properties(tm, orc):
+    """Config-2 width at a large row count: sampled rows vs the oracle, and
+    size-independent properties on all rows (finite, masked rows zero, each
+    row's gradient sums to ~0 since sum_v (onehot - p) = 0)."""
+    from paper_2604_11554_b200 import _lib
+
+    T, V = 8192, 151936
+    logits = torch.empty(T, V, dtype=torch.bfloat16, device="cuda")
+    g = torch.Generator(device="cpu").manual_seed(0)
+    peak = torch.randint(0, V, (T,), generator=g).to(torch.int32).cuda()
+    tm.synth_logits(logits, seed=1234, sigma=2.0, peak_id=peak)
+    targets = torch.where(torch.rand(T, generator=g).cuda() < 0.5, peak,
+                          torch.randint(0, V, (T,), generator=g).to(torch.int32).cuda()).to(torch.int32)
+    logp0, _, _ = tm.logprob_fwd(logits, targets)
+    old = (logp0 + 0.05 * torch.randn(T, generator=g).cuda()).float()
+    ref = (logp0 + 0.1 * torch.randn(T, generator=g).cuda()).float()
+    adv_tok = torch.randn(T, generator=g).cuda()
+    w_tok = (torch.rand(T, generator=g).cuda() < 0.9).float() / T
+    met, dl, logp, ent = tm.pg_loss_fwd_bwd(logits, targets, old, ref, adv_tok, w_tok, want_logp=True)
+    torch.cuda.synchronize()
+    act = (w_tok != 0)
+    assert torch.all(dl[~act] == 0)
+    rs = dl.float().sum(1)
+    assert torch.all(rs.abs() <= 2e-3 * (torch.abs(w_tok) * 4 * (adv_tok.abs() + 1)) + 1e-7)
+    assert torch.isfinite(met).all()
+    assert met[_lib.NUM_METRICS - 2].item() == act.sum().item()
+    rows = torch.randperm(T, generator=g)[:12].sort().values
+    sub = logits[rows.cuda()].contiguous()
+    sub_bits = sub.view(torch.int16).cpu().numpy().view(np.uint16)
+    tg = targets[rows.cuda()].cpu().numpy()
+    a = adv_tok[rows.cuda()].cpu().numpy()
+    w = w_tok[rows.cuda()].cpu().numpy()
+    o, r = old[rows.cuda()].cpu().numpy(), ref[rows.cuda()].cpu().numpy()
+    om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(sub_bits, tg, o, r, a, w)
+    actn = w != 0
+    assert_close(logp[rows.cuda()].cpu().numpy()[actn], olp[actn], what="logp")
+    assert_close(ent[rows.cuda()].cpu().numpy()[actn], oent[actn], what="entropy")
+    near = near_clip_rows(olp, o, a, 0.2, 0.28)
+    assert_grad_close(grad_to_np(dl[rows.cuda()]), odl, np.abs(og), "bf16", rows_ok=~near)
+    # metrics self-consistency: recompute sum w*H from per-row outputs
+    wh = float((w_tok.double() * ent.double()).sum())
+    assert abs(met[3].item() - wh) <= 1e-5 * abs(wh) + 1e-6
