@@ -1,0 +1,575 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// The fused hot path (SURVEY.md §8 rows a1 + a4 + a2): per token, the vocab-wide
+// log-softmax gather (logp, entropy), the DAPO/GRPO surrogate with optional KL
+// and entropy bonus, and the dlogits backward — in ONE pass over HBM: each
+// logits row is read once and its gradient written once (4V bytes per
+// loss-active bf16 token).
+//
+// sm_100a structure (one CTA per SM, a C-CTA cluster per row, persistent):
+//
+//   warp 16        TMA producer: cp.async.bulk 8 KB chunks of this CTA's row
+//                  slice into a 26-slot shared-memory ring (mbarrier
+//                  complete_tx), running ahead across rows.
+//   warps 0..7     FORWARD: read a chunk from smem, release the smem slot at
+//                  once, stash the raw words in TENSOR MEMORY (tcgen05.st,
+//                  32 slots x 8 KB = the whole 256 KB TMEM) and fold them into
+//                  the online (max, sum, weighted-sum) softmax state. At the
+//                  end of a row: CTA reduction, then the partial statistics go
+//                  to every CTA of the cluster through DSMEM mailboxes with
+//                  remote mbarrier arrives.
+//   warps 8..15    BACKWARD: wait for the row's merged statistics, compute the
+//                  per-token loss scalars, then re-read the row from TMEM
+//                  (tcgen05.ld), form dlogits and stream them to HBM.
+//
+// TMEM is the row store that makes single-pass possible: a Qwen3 bf16 row
+// (303,872 B) split over a 2-CTA cluster is 152 KB per SM, which fits TMEM
+// with 13 chunks of slack, so the forward warps run up to ~0.7 rows ahead of
+// the backward warps and both overlap the TMA stream. Each backward warp reads
+// exactly the TMEM lanes/columns its partner forward warp (same SM
+// sub-partition, warp b = f + 8) wrote, so TMEM needs no cross-lane layout.
+//
+// Reference seam replaced: trainer_compute_batch latency (proj/src/sim_runtime.cpp:441)
+// and trainer_thread sleep (proj/src/wall_runtime.cpp:197); math pinned in
+// DESIGN.md §2, fp64 twin oracle/sf_oracle.c orc_pg_loss_fwd_bwd.
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "tm_rowmath.cuh"
+
+namespace sftm {
+
+namespace loss {
+
+constexpr int kFW = 8;                      // forward warps
+constexpr int kBW = 8;                      // backward warps
+constexpr int kFT = kFW * 32;               // 256 forward threads
+constexpr int kProd = kFW + kBW;            // producer warp index
+constexpr int kThreads = (kFW + kBW + 1) * 32;
+constexpr int kCB = 8192;                   // chunk bytes (smem slot and TMEM slot)
+constexpr int kSlots = 26;                  // smem ring slots
+constexpr int kRingBytes = kSlots * kCB;    // 212,992 B
+constexpr int kTSlots = 32;                 // TMEM slots of 16 columns (8 KB)
+constexpr int kTCols = 512;
+constexpr int kMailD = 8;                   // mailbox ring depth (rows)
+constexpr int kMaxChunks = 20;              // row-slice chunks that keep >= 12 TMEM slots free
+
+template <typename T>
+struct Geo {
+  static constexpr int es = sizeof(T);
+  static constexpr int CE = kCB / es;       // elements per chunk
+  static constexpr int HALF = CE / 2;       // second 16-B vector of a thread starts here
+  static constexpr int EV = 16 / es;        // elements per 16-B vector
+  static constexpr int NE = 2 * EV;         // elements per thread per chunk
+};
+
+// 8 words (two 16-B vectors) -> NE floats
+__device__ __forceinline__ void unpack(const float*, uint4 a, uint4 b, float (&x)[8]) {
+  x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
+  x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+  x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
+  x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+}
+__device__ __forceinline__ void unpack(const uint16_t*, uint4 a, uint4 b, float (&x)[16]) {
+  x[0] = bf16lo(a.x); x[1] = bf16hi(a.x); x[2] = bf16lo(a.y); x[3] = bf16hi(a.y);
+  x[4] = bf16lo(a.z); x[5] = bf16hi(a.z); x[6] = bf16lo(a.w); x[7] = bf16hi(a.w);
+  x[8] = bf16lo(b.x); x[9] = bf16hi(b.x); x[10] = bf16lo(b.y); x[11] = bf16hi(b.y);
+  x[12] = bf16lo(b.z); x[13] = bf16hi(b.z); x[14] = bf16lo(b.w); x[15] = bf16hi(b.w);
+}
+
+// Element offset (within a chunk) of a thread's j-th element.
+template <typename T>
+__device__ __forceinline__ int elem_off(int tid, int j) {
+  using G = Geo<T>;
+  return (j < G::EV) ? (G::EV * tid + j) : (G::HALF + G::EV * tid + (j - G::EV));
+}
+
+// Online update with N elements; no clamp: a -inf logit makes w NaN, which the
+// caller repairs on a slow path (logits from an LM head are finite).
+template <int N>
+__device__ __forceinline__ void accum(Stats& st, const float (&x)[N], float c) {
+  float xm = x[0];
+#pragma unroll
+  for (int j = 1; j < N; ++j) xm = fmaxf(xm, x[j]);
+  const float cm = xm * c;
+  if (cm > st.m2) {
+    if (st.m2 != -INFINITY) {
+      const float d = st.m2 - cm;
+      const float f = ex2(d);
+      st.w = f * fmaf(st.s, d, st.w);
+      st.s *= f;
+    }
+    st.m2 = cm;
+  }
+  float s[4] = {0.f, 0.f, 0.f, 0.f}, w[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float a = fmaf(x[j], c, -st.m2);
+    const float e = ex2(a);
+    s[j & 3] += e;
+    w[j & 3] = fmaf(e, a, w[j & 3]);
+  }
+  st.s += (s[0] + s[1]) + (s[2] + s[3]);
+  st.w += (w[0] + w[1]) + (w[2] + w[3]);
+}
+
+// Careful (slow) variant: masked elements and -inf logits contribute nothing.
+template <int N>
+__device__ __forceinline__ void accum_masked(Stats& st, const float (&x)[N], const bool (&ok)[N],
+                                             float c) {
+  float xm = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (ok[j]) xm = fmaxf(xm, x[j]);
+  const float cm = xm * c;
+  if (cm > st.m2) {
+    if (st.m2 != -INFINITY) {
+      const float d = st.m2 - cm;
+      const float f = ex2(d);
+      st.w = f * fmaf(st.s, d, st.w);
+      st.s *= f;
+    }
+    st.m2 = cm;
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (ok[j] && x[j] != -INFINITY) {
+      const float a = fmaf(x[j], c, -st.m2);
+      const float e = ex2(a);
+      st.s += e;
+      st.w = fmaf(e, a, st.w);
+    }
+  }
+}
+
+__device__ __forceinline__ void store_vec(float* p, const float* g) {
+  stg128_cs(p, make_uint4(__float_as_uint(g[0]), __float_as_uint(g[1]), __float_as_uint(g[2]),
+                          __float_as_uint(g[3])));
+}
+__device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
+  stg128_cs(p, make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]),
+                          pack_bf16x2(g[4], g[5]), pack_bf16x2(g[6], g[7])));
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(kThreads, 1)
+    loss_tmem_kernel(const RowArgs a, int64_t slice_elems) {
+  using G = Geo<T>;
+  constexpr int CE = G::CE;
+  constexpr int NE = G::NE;
+  constexpr int EV = G::EV;
+
+  extern __shared__ __align__(1024) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full_bar[kSlots];
+  __shared__ __align__(8) uint64_t empty_bar[kSlots];
+  __shared__ __align__(8) uint64_t tfull_bar[kTSlots];
+  __shared__ __align__(8) uint64_t tempty_bar[kTSlots];
+  __shared__ __align__(8) uint64_t mail_bar[kMailD];
+  __shared__ __align__(16) float4 mail[kMailD][8];
+  __shared__ __align__(16) float4 red[2][kFW];
+  __shared__ float zyv[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const uint32_t crank = (C > 1) ? cluster_ctarank() : 0u;
+  const int64_t cid = (C > 1) ? static_cast<int64_t>(cluster_id_x()) : blockIdx.x;
+  const int64_t ncl = (C > 1) ? static_cast<int64_t>(nclusters_x()) : gridDim.x;
+  const int64_t slice_start = static_cast<int64_t>(crank) * slice_elems;
+  int64_t sl64 = a.V - slice_start;
+  if (sl64 > slice_elems) sl64 = slice_elems;
+  if (sl64 < 0) sl64 = 0;
+  const int slice_len = static_cast<int>(sl64);
+  const int nck = (slice_len + CE - 1) / CE;
+  const int nfull = slice_len / CE;
+  const uint32_t ring_base = smem_u32(ring);
+
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), kFW);
+    }
+    for (int i = 0; i < kTSlots; ++i) {
+      mbar_init(smem_u32(&tfull_bar[i]), kFW);
+      mbar_init(smem_u32(&tempty_bar[i]), kBW);
+    }
+    for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
+    zyv[0] = zyv[1] = __int_as_float(0x7fc00000);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_base_sh), kTCols);
+  tc_fence_before();
+  if (C > 1) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
+  tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  const T* logits = static_cast<const T*>(a.logits);
+
+  if (warp == kProd) {
+    // ================================================================ producer
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      uint32_t slot = 0, ph = 0;
+      for (int64_t t = cid; t < a.T; t += ncl) {
+        if (__ldg(a.w_tok + t) == 0.f) continue;
+        const T* row = logits + t * a.ld + slice_start;
+        for (int k = 0; k < nck; ++k) {
+          const int rem = slice_len - k * CE;
+          const uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
+          mbar_wait(smem_u32(&empty_bar[slot]), ph ^ 1u);
+          mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes);
+          bulk_g2s(ring_base + slot * kCB, row + static_cast<int64_t>(k) * CE, bytes,
+                   smem_u32(&full_bar[slot]), pol);
+          if (++slot == kSlots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kFW) {
+    // ================================================================ forward
+    const int ftid = tid;                      // 0..255
+    const uint32_t tlane = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const uint32_t tcol = 8u * static_cast<uint32_t>(warp >> 2);
+    const float c = a.inv_tau * kLog2e;
+    uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
+    for (int64_t t = cid; t < a.T; t += ncl) {
+      if (__ldg(a.w_tok + t) == 0.f) continue;
+      const int64_t yl = static_cast<int64_t>(__ldg(a.targets + t)) - a.vocab_start - slice_start;
+      int ck = -1, jt = 0;
+      if (yl >= 0 && yl < slice_len) {
+        const int r = static_cast<int>(yl % CE);
+        const int v = r >= G::HALF ? 1 : 0;
+        const int rr = r - v * G::HALF;
+        if (rr / EV == ftid) {
+          ck = static_cast<int>(yl / CE);
+          jt = v * EV + rr % EV;
+        }
+      }
+      Stats my = stats_empty();
+      const uint32_t ts0 = ts;
+      for (int k = 0; k < nck; ++k) {
+        mbar_wait(smem_u32(&full_bar[slot]), ph);
+        const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
+        const uint4 v0 = lds128(sa);
+        const uint4 v1 = lds128(sa + kCB / 2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
+        if (++slot == kSlots) {
+          slot = 0;
+          ph ^= 1u;
+        }
+        // stash the raw words in TMEM for the backward warps
+        mbar_wait(smem_u32(&tempty_bar[ts]), tph ^ 1u);
+        tc_fence_after();
+        tmem_st8(tbase + tlane + ts * 16u + tcol, v0, v1);
+        float x[NE];
+        unpack(logits, v0, v1, x);
+        if (k == ck) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            if (j == jt) zyv[nrow & 1] = x[j] * a.inv_tau;
+        }
+        if (k < nfull) {
+          accum(my, x, c);
+        } else {
+          const int rem = slice_len - k * CE;
+          bool ok[NE];
+#pragma unroll
+          for (int j = 0; j < NE; ++j) ok[j] = elem_off<T>(ftid, j) < rem;
+          accum_masked(my, x, ok, c);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tfull_bar[ts]));
+        if (++ts == kTSlots) {
+          ts = 0;
+          tph ^= 1u;
+        }
+      }
+      // -inf logits made w NaN: recompute this warp's w from its TMEM words.
+      if (__any_sync(0xffffffffu, my.w != my.w)) {
+        float wr = 0.f;
+        uint32_t q = ts0;
+        for (int k = 0; k < nck; ++k) {
+          uint4 v0, v1;
+          tmem_ld8(tbase + tlane + q * 16u + tcol, v0, v1);
+          tmem_wait_ld();
+          float x[NE];
+          unpack(logits, v0, v1, x);
+          const int rem = slice_len - k * CE;
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
+              const float av = fmaf(x[j], c, -my.m2);
+              wr = fmaf(ex2(av), av, wr);
+            }
+          }
+          if (++q == kTSlots) q = 0;
+        }
+        my.w = wr;
+      }
+      // CTA reduction of the forward partials, then DSMEM mailbox broadcast.
+      my = warp_merge(my);
+      const uint32_t b2 = nrow & 1u;
+      if (lane == 0) red[b2][warp] = make_float4(my.m2, my.s, my.w, 0.f);
+      named_bar_sync(1, kFT);
+      if (warp == 0) {
+        Stats v = stats_empty();
+        if (lane < kFW) {
+          const float4 r = red[b2][lane];
+          v = Stats{r.x, r.y, r.z};
+        }
+        v = warp_merge(v);
+        if (lane == 0) {
+          const float z = zyv[b2];
+          zyv[b2] = __int_as_float(0x7fc00000);
+          const uint32_t mb = nrow % kMailD;
+          if (C == 1) {
+            mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
+            mbar_arrive(smem_u32(&mail_bar[mb]));
+          } else {
+            const uint32_t my_slot = smem_u32(&mail[mb][crank]);
+            const uint32_t my_bar = smem_u32(&mail_bar[mb]);
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+              st_cluster_v4(mapa(my_slot, q), v.m2, v.s, v.w, z);
+              mbar_arrive_remote(mapa(my_bar, q));
+            }
+          }
+        }
+      }
+      ++nrow;
+    }
+  } else {
+    // ================================================================ backward
+    const int btid = tid - kFT;               // same element mapping as forward warp (warp-8)
+    const int fw = warp - kFW;
+    const uint32_t tlane = static_cast<uint32_t>(32 * (fw & 3)) << 16;
+    const uint32_t tcol = 8u * static_cast<uint32_t>(fw >> 2);
+    const float c = a.inv_tau * kLog2e;
+    const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
+    const bool leader = (crank == 0 && btid == 0);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t ts = 0, tph = 0, nrow = 0;
+    for (int64_t t = cid; t < a.T; t += ncl) {
+      const float w = __ldg(a.w_tok + t);
+      if (w == 0.f) {
+        if (!a.masked_skip) {
+          uint8_t* drow = reinterpret_cast<uint8_t*>(static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start);
+          const int nb = slice_len * G::es;
+          for (int off = btid * 16; off < nb; off += kFT * 16) stg128_cs(drow + off, make_uint4(0, 0, 0, 0));
+        }
+        if (leader) {
+          if (a.out_logp) a.out_logp[t] = 0.f;
+          if (a.out_entropy) a.out_entropy[t] = 0.f;
+        }
+        continue;
+      }
+      const float A = __ldg(a.adv_tok + t);
+      const float old = __ldg(a.old_logp + t);
+      const float ref = __ldg(a.ref_logp + t);
+      const int64_t yl = static_cast<int64_t>(__ldg(a.targets + t)) - a.vocab_start - slice_start;
+      const uint32_t mb = nrow % kMailD;
+      if (C == 1) {
+        mbar_wait(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
+      } else {
+        mbar_wait_cluster(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
+      }
+      Stats st = stats_empty();
+      float zy = __int_as_float(0x7fc00000);
+#pragma unroll
+      for (int q = 0; q < C; ++q) {
+        const float4 mv = mail[mb][q];
+        st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
+        if (!(mv.w != mv.w)) zy = mv.w;
+      }
+      float lse2, lse, H, logp;
+      row_scalars(st, zy, lse2, lse, H, logp);
+      float g, gH, m[8];
+      loss_terms(logp, H, w, A, old, ref, P, g, gH, m);
+      if (leader) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(m[i]);
+        if (a.out_logp) a.out_logp[t] = logp;
+        if (a.out_entropy) a.out_entropy[t] = H;
+      }
+      // dlogits_v = gt*[v==y] - p_v*(c0 + c1*a_v), a_v = (z_v - lse)*log2e, p_v = 2^a_v.
+      const float gt = a.inv_tau * g;
+      const float c0 = a.inv_tau * (g + gH * H);
+      const float c1 = a.inv_tau * gH * kLn2;
+      // Fast form (c1 == 0): p_v*c0 = sign(c0) * 2^(a_v + log2|c0|).
+      const float lse2f = lse2 - log2f(fabsf(c0));
+      const bool neg = c0 > 0.f;  // gradient entries are -p*c0
+      int ck = -1, jt = 0;
+      if (yl >= 0 && yl < slice_len) {
+        const int r = static_cast<int>(yl % CE);
+        const int v = r >= G::HALF ? 1 : 0;
+        const int rr = r - v * G::HALF;
+        if (rr / EV == btid) {
+          ck = static_cast<int>(yl / CE);
+          jt = v * EV + rr % EV;
+        }
+      }
+      T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
+      for (int k = 0; k < nck; ++k) {
+        mbar_wait(smem_u32(&tfull_bar[ts]), tph);
+        tc_fence_after();
+        uint4 v0, v1;
+        tmem_ld8(tbase + tlane + ts * 16u + tcol, v0, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[ts]));
+        if (++ts == kTSlots) {
+          ts = 0;
+          tph ^= 1u;
+        }
+        float x[NE], gr[NE];
+        unpack(logits, v0, v1, x);
+        if (G::es == 2 && c1 == 0.f) {
+          // bf16 output: fold |c0| into the exponent (one MUFU, no FMUL)
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            const float e = ex2(fmaf(x[j], c, -lse2f));
+            gr[j] = neg ? -e : e;
+          }
+        } else if (c1 == 0.f) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j) gr[j] = -ex2(fmaf(x[j], c, -lse2)) * c0;
+        } else {
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            const float av = fmaxf(fmaf(x[j], c, -lse2), -127.f);
+            gr[j] = -ex2(av) * fmaf(c1, av, c0);
+          }
+        }
+        if (k == ck) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            if (j == jt) gr[j] += gt;
+        }
+        T* dst = drow + k * CE;
+        if (k < nfull) {
+          store_vec(dst + EV * btid, gr);
+          store_vec(dst + G::HALF + EV * btid, gr + EV);
+        } else {
+          const int rem = slice_len - k * CE;
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            const int off = elem_off<T>(btid, j);
+            if (off < rem) st1(dst + off, gr[j]);
+          }
+        }
+      }
+      ++nrow;
+    }
+    if (leader) finish_metrics(a, cid, ncl, acc);
+  }
+
+  // teardown: every TMEM access is complete before warp 0 frees it
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, kTCols);
+  if (C > 1) cluster_sync_all();
+}
+
+std::mutex g_mu;
+
+template <typename T, int C>
+int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
+  auto kern = loss_tmem_kernel<T, C>;
+  static int max_active = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (max_active < 0) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
+      if (e != cudaSuccess) return e;
+      if (C > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C * 256);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kRingBytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) return e;
+        max_active = n;
+      } else {
+        int per_sm = 0, dev = 0, sms = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kRingBytes);
+        if (e != cudaSuccess) return e;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        max_active = per_sm * sms;
+      }
+      if (max_active <= 0) return cudaErrorInvalidConfiguration;
+    }
+  }
+  int64_t ncl = a.T < max_active ? a.T : max_active;
+  if (ncl > a.max_partial_blocks) ncl = a.max_partial_blocks;
+  if (ncl < 1) ncl = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(ncl * C));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kRingBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (C > 1) ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, slice);
+  if (info) {
+    info->kernel = 2;
+    info->cluster = C;
+    info->grid = static_cast<int>(ncl * C);
+    info->launches = 1;
+  }
+  return e;
+}
+
+template <typename T>
+int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
+  using G = Geo<T>;
+  for (int C : {1, 2, 4, 8}) {
+    int64_t slice = (a.V + C - 1) / C;
+    slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
+    const int64_t nck = (slice + G::CE - 1) / G::CE;
+    if (nck > kMaxChunks) continue;
+    switch (C) {
+      case 1: return launch_c<T, 1>(a, slice, s, info);
+      case 2: return launch_c<T, 2>(a, slice, s, info);
+      case 4: return launch_c<T, 4>(a, slice, s, info);
+      case 8: return launch_c<T, 8>(a, slice, s, info);
+    }
+  }
+  return -2;  // not eligible: caller falls back
+}
+
+}  // namespace loss
+
+int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
+  if (a.dtype == 1) return loss::launch_t<uint16_t>(a, s, info);
+  return loss::launch_t<float>(a, s, info);
+}
+
+}  // namespace sftm

@@ -103,7 +103,7 @@ def check_loss_case(tm, orc, prob, pkw=None, generic=False, in_place=False, mask
             if name == "n_active":
                 assert gm[i] == om[i]
             else:
-                t = tol * (30 if name in ("kl", "entropy") else 1)
+                t = tol * (30 if name in ("kl", "entropy") else 1) + 1e-5 * abs(om[i])
                 assert abs(gm[i] - om[i]) <= t, (name, gm[i], om[i])
     return gm, gdl
 
