@@ -34,11 +34,28 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// try_wait suspend-time hint: a waiting warp sleeps in hardware until the phase
+// completes (or this many ns pass) instead of re-issuing probes through MIO.
+constexpr uint32_t kSuspendNs = 1000000u;
+
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(kSuspendNs)
+      : "memory");
+  return ok != 0;
+}
+
+// Non-blocking probe of a phase (mbarrier.test_wait never suspends the thread).
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(bar), "r"(parity)
@@ -57,10 +74,10 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(kSuspendNs)
       : "memory");
   return ok != 0;
 }
@@ -68,6 +85,25 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait_cluster(bar, parity)) {
   }
+}
+
+// Cheaper cluster wait: spin relaxed (no per-probe L1 invalidation), then one
+// acquire fence restricted to shared::cluster (the DSMEM mailbox).
+__device__ __forceinline__ bool mbar_try_wait_relaxed_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(kSuspendNs)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster_lite(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait_relaxed_cluster(bar, parity)) {
+  }
+  asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
@@ -175,6 +211,13 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
 __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// wait::st that also keeps the stored source registers alive until completion
+__device__ __forceinline__ void tmem_wait_st(uint4& a, uint4& b) {
+  asm volatile("tcgen05.wait::st.sync.aligned;"
+               : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w)
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint4& a, uint4& b) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -184,6 +227,13 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint4& a, uint4& b) {
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// wait::ld tied to the destination registers so no use is scheduled before it
+__device__ __forceinline__ void tmem_wait_ld(uint4& a, uint4& b) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w)
+               :
+               : "memory");
 }
 
 // ---------------------------------------------------------------- math

@@ -43,18 +43,19 @@ namespace sftm {
 
 namespace loss {
 
-constexpr int kFW = 8;                      // forward warps
-constexpr int kBW = 8;                      // backward warps
-constexpr int kFT = kFW * 32;               // 256 forward threads
+constexpr int kFW = 12;                     // forward warps (3 per SM sub-partition)
+constexpr int kBW = 12;                     // backward warps (3 per SM sub-partition)
+constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
-constexpr int kThreads = (kFW + kBW + 1) * 32;
-constexpr int kCB = 8192;                   // chunk bytes (smem slot and TMEM slot)
-constexpr int kSlots = 26;                  // smem ring slots
-constexpr int kRingBytes = kSlots * kCB;    // 212,992 B
-constexpr int kTSlots = 32;                 // TMEM slots of 16 columns (8 KB)
+constexpr int kThreads = (kFW + kBW + 1) * 32;  // 800
+constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per thread = 12 KB
+constexpr int kSlots = 17;                  // smem ring slots (204 KB)
+constexpr int kRingBytes = kSlots * kCB;
+constexpr int kSlotCols = kCB / (128 * 4);  // TMEM columns per chunk slot (24)
+constexpr int kTSlots = 512 / kSlotCols;    // 21 TMEM chunk slots (252 KB)
 constexpr int kTCols = 512;
 constexpr int kMailD = 8;                   // mailbox ring depth (rows)
-constexpr int kMaxChunks = 20;              // row-slice chunks that keep >= 12 TMEM slots free
+constexpr int kMaxChunks = 14;              // row-slice chunks that keep >= 7 TMEM slots free
 
 template <typename T>
 struct Geo {
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================================================================ forward
     const int ftid = tid;                      // 0..255
     const uint32_t tlane = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-    const uint32_t tcol = 8u * static_cast<uint32_t>(warp >> 2);
+    const uint32_t tcol = 8u * static_cast<uint32_t>(warp >> 2);  // 8 columns per warp of a sub-partition
     const float c = a.inv_tau * kLog2e;
     uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
     for (int64_t t = cid; t < a.T; t += ncl) {
@@ -254,23 +255,55 @@ __global__ void __launch_bounds__(kThreads, 1)
           jt = v * EV + rr % EV;
         }
       }
-      Stats my = stats_empty();
+      // online state with 4 independent partial sums (ILP), kept across chunks
+      float m2 = -INFINITY;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
       const uint32_t ts0 = ts;
-      for (int k = 0; k < nck; ++k) {
+      uint4 v0, v1, n0 = make_uint4(0, 0, 0, 0), n1 = make_uint4(0, 0, 0, 0);
+      {
         mbar_wait(smem_u32(&full_bar[slot]), ph);
         const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
-        const uint4 v0 = lds128(sa);
-        const uint4 v1 = lds128(sa + kCB / 2);
+        v0 = lds128(sa);
+        v1 = lds128(sa + kCB / 2);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
         if (++slot == kSlots) {
           slot = 0;
           ph ^= 1u;
         }
+      }
+      {
+        // base of the row's exponent arguments: this thread's max of chunk 0.
+        // Later elements may exceed it (arguments > 0 are fine); only a jump
+        // of > 126 in log2 units overflows, which the row-end repair handles.
+        float x[NE];
+        unpack(logits, v0, v1, x);
+        float xm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < NE; ++j)
+          if (elem_off<T>(ftid, j) < slice_len) xm = fmaxf(xm, x[j]);
+        m2 = xm * c;
+        if (!(m2 > -INFINITY)) m2 = 0.f;  // nothing finite: any finite base works
+      }
+      for (int k = 0; k < nck; ++k) {
+        // opportunistic prefetch of the next chunk (only if it has already landed)
+        bool have_next = false;
+        if (k + 1 < nck && mbar_test(smem_u32(&full_bar[slot]), ph)) {
+          const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
+          n0 = lds128(sa);
+          n1 = lds128(sa + kCB / 2);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
+          if (++slot == kSlots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+          have_next = true;
+        }
         // stash the raw words in TMEM for the backward warps
         mbar_wait(smem_u32(&tempty_bar[ts]), tph ^ 1u);
         tc_fence_after();
-        tmem_st8(tbase + tlane + ts * 16u + tcol, v0, v1);
+        tmem_st8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
         float x[NE];
         unpack(logits, v0, v1, x);
         if (k == ck) {
@@ -279,15 +312,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == jt) zyv[nrow & 1] = x[j] * a.inv_tau;
         }
         if (k < nfull) {
-          accum(my, x, c);
-        } else {
-          const int rem = slice_len - k * CE;
-          bool ok[NE];
 #pragma unroll
-          for (int j = 0; j < NE; ++j) ok[j] = elem_off<T>(ftid, j) < rem;
-          accum_masked(my, x, ok, c);
+          for (int j = 0; j < NE; ++j) {
+            const float av = fmaf(x[j], c, -m2);
+            const float e = ex2(av);
+            s4[j & 3] += e;
+            w4[j & 3] = fmaf(e, av, w4[j & 3]);
+          }
+        } else {
+          // last (partial) chunk of the slice: masked, -inf safe
+          const int rem = slice_len - k * CE;
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
+              const float av = fmaf(x[j], c, -m2);
+              const float e = ex2(av);
+              s4[0] += e;
+              w4[0] = fmaf(e, av, w4[0]);
+            }
+          }
         }
-        tmem_wait_st();
+        tmem_wait_st(v0, v1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tfull_bar[ts]));
@@ -295,29 +340,65 @@ __global__ void __launch_bounds__(kThreads, 1)
           ts = 0;
           tph ^= 1u;
         }
+        if (k + 1 < nck && !have_next) {
+          mbar_wait(smem_u32(&full_bar[slot]), ph);
+          const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
+          n0 = lds128(sa);
+          n1 = lds128(sa + kCB / 2);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
+          if (++slot == kSlots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+        v0 = n0;
+        v1 = n1;
       }
-      // -inf logits made w NaN: recompute this warp's w from its TMEM words.
-      if (__any_sync(0xffffffffu, my.w != my.w)) {
-        float wr = 0.f;
+      Stats my{m2, (s4[0] + s4[1]) + (s4[2] + s4[3]), (w4[0] + w4[1]) + (w4[2] + w4[3])};
+      // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
+      // (a logit > 126/log2e above the chunk-0 base) made s or w non-finite:
+      // recompute this thread's partials exactly from its TMEM words.
+      const bool bad = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f);
+      if (__any_sync(0xffffffffu, bad)) {
+        float mx = -INFINITY;
         uint32_t q = ts0;
         for (int k = 0; k < nck; ++k) {
-          uint4 v0, v1;
-          tmem_ld8(tbase + tlane + q * 16u + tcol, v0, v1);
-          tmem_wait_ld();
+          uint4 v0r, v1r;
+          tmem_ld8(tbase + tlane + q * static_cast<uint32_t>(kSlotCols) + tcol, v0r, v1r);
+          tmem_wait_ld(v0r, v1r);
           float x[NE];
-          unpack(logits, v0, v1, x);
+          unpack(logits, v0r, v1r, x);
+          const int rem = slice_len - k * CE;
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            if (elem_off<T>(ftid, j) < rem) mx = fmaxf(mx, x[j]);
+          if (++q == kTSlots) q = 0;
+        }
+        const float mb2 = (mx == -INFINITY) ? -INFINITY : mx * c;
+        float sr = 0.f, wr = 0.f;
+        q = ts0;
+        for (int k = 0; k < nck; ++k) {
+          uint4 v0r, v1r;
+          tmem_ld8(tbase + tlane + q * static_cast<uint32_t>(kSlotCols) + tcol, v0r, v1r);
+          tmem_wait_ld(v0r, v1r);
+          float x[NE];
+          unpack(logits, v0r, v1r, x);
           const int rem = slice_len - k * CE;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
             if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
-              const float av = fmaf(x[j], c, -my.m2);
-              wr = fmaf(ex2(av), av, wr);
+              const float av = fmaf(x[j], c, -mb2);
+              const float e = ex2(av);
+              sr += e;
+              wr = fmaf(e, av, wr);
             }
           }
           if (++q == kTSlots) q = 0;
         }
-        my.w = wr;
+        if (bad) my = Stats{mb2, sr, wr};
       }
+      if (my.s == 0.f) my = stats_empty();  // nothing finite in this thread's share
       // CTA reduction of the forward partials, then DSMEM mailbox broadcast.
       my = warp_merge(my);
       const uint32_t b2 = nrow & 1u;
@@ -383,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (C == 1) {
         mbar_wait(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
       } else {
-        mbar_wait_cluster(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
+        mbar_wait_cluster_lite(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
       }
       Stats st = stats_empty();
       float zy = __int_as_float(0x7fc00000);
@@ -421,45 +502,97 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
+      const uint32_t sgn = neg ? 0x80008000u : 0u;
+      const float gts = neg ? -gt : gt;  // target term before the sign flip
+      uint4 v0, v1;
+      uint32_t cur = ts;
+      mbar_wait(smem_u32(&tfull_bar[ts]), tph);
+      tc_fence_after();
+      tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
+      if (++ts == kTSlots) {
+        ts = 0;
+        tph ^= 1u;
+      }
+      bool pending = true;  // a TMEM load for chunk k is in flight
       for (int k = 0; k < nck; ++k) {
-        mbar_wait(smem_u32(&tfull_bar[ts]), tph);
-        tc_fence_after();
-        uint4 v0, v1;
-        tmem_ld8(tbase + tlane + ts * 16u + tcol, v0, v1);
-        tmem_wait_ld();
+        if (!pending) {
+          mbar_wait(smem_u32(&tfull_bar[ts]), tph);
+          tc_fence_after();
+          tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
+          cur = ts;
+          if (++ts == kTSlots) {
+            ts = 0;
+            tph ^= 1u;
+          }
+        }
+        tmem_wait_ld(v0, v1);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[ts]));
-        if (++ts == kTSlots) {
-          ts = 0;
-          tph ^= 1u;
-        }
-        float x[NE], gr[NE];
-        unpack(logits, v0, v1, x);
-        if (G::es == 2 && c1 == 0.f) {
-          // bf16 output: fold |c0| into the exponent (one MUFU, no FMUL)
-#pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const float e = ex2(fmaf(x[j], c, -lse2f));
-            gr[j] = neg ? -e : e;
+        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[cur]));
+        const uint4 w0 = v0, w1 = v1;
+        bool have_next = false;
+        if (k + 1 < nck && mbar_test(smem_u32(&tfull_bar[ts]), tph)) {
+          // next chunk already stashed: start its TMEM load before computing this one
+          tc_fence_after();
+          tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
+          cur = ts;
+          if (++ts == kTSlots) {
+            ts = 0;
+            tph ^= 1u;
           }
+          have_next = true;
+        }
+        pending = have_next;
+        float x[NE], gr[NE];
+        unpack(logits, w0, w1, x);
+        T* dst = drow + k * CE;
+        const bool full = k < nfull;
+        if (G::es == 2 && c1 == 0.f) {
+          // bf16: |c0| folded into the exponent, sign applied on the packed words
+#pragma unroll
+          for (int j = 0; j < NE; ++j) gr[j] = ex2(fmaf(x[j], c, -lse2f));
+          if (k == ck) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j)
+              if (j == jt) gr[j] += gts;
+          }
+          if (full) {
+            uint4 p0, p1;
+            p0.x = pack_bf16x2(gr[0], gr[1]) ^ sgn;
+            p0.y = pack_bf16x2(gr[2], gr[3]) ^ sgn;
+            p0.z = pack_bf16x2(gr[4], gr[5]) ^ sgn;
+            p0.w = pack_bf16x2(gr[6], gr[7]) ^ sgn;
+            p1.x = pack_bf16x2(gr[8], gr[9]) ^ sgn;
+            p1.y = pack_bf16x2(gr[10], gr[11]) ^ sgn;
+            p1.z = pack_bf16x2(gr[12], gr[13]) ^ sgn;
+            p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
+            stg128_cs(dst + EV * btid, p0);
+            stg128_cs(dst + G::HALF + EV * btid, p1);
+            continue;
+          }
+#pragma unroll
+          for (int j = 0; j < NE; ++j) gr[j] = neg ? -gr[j] : gr[j];
         } else if (c1 == 0.f) {
 #pragma unroll
           for (int j = 0; j < NE; ++j) gr[j] = -ex2(fmaf(x[j], c, -lse2)) * c0;
+          if (k == ck) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j)
+              if (j == jt) gr[j] += gt;
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
             const float av = fmaxf(fmaf(x[j], c, -lse2), -127.f);
             gr[j] = -ex2(av) * fmaf(c1, av, c0);
           }
-        }
-        if (k == ck) {
+          if (k == ck) {
 #pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (j == jt) gr[j] += gt;
+            for (int j = 0; j < NE; ++j)
+              if (j == jt) gr[j] += gt;
+          }
         }
-        T* dst = drow + k * CE;
-        if (k < nfull) {
+        if (full) {
           store_vec(dst + EV * btid, gr);
           store_vec(dst + G::HALF + EV * btid, gr + EV);
         } else {
