@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
-      mbar_init(smem_u32(&empty_bar[i]), kFW);
+      mbar_init(smem_u32(&empty_bar[i]), kFT);  // every forward thread arrives
     }
     for (int i = 0; i < kTSlots; ++i) {
-      mbar_init(smem_u32(&tfull_bar[i]), kFW);
-      mbar_init(smem_u32(&tempty_bar[i]), kBW);
+      mbar_init(smem_u32(&tfull_bar[i]), kFT);
+      mbar_init(smem_u32(&tempty_bar[i]), kFT);  // backward threads (same count)
     }
     for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
     zyv[0] = zyv[1] = __int_as_float(0x7fc00000);
@@ -241,6 +241,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tlane = static_cast<uint32_t>(32 * (warp & 3)) << 16;
     const uint32_t tcol = 8u * static_cast<uint32_t>(warp >> 2);  // 8 columns per warp of a sub-partition
     const float c = a.inv_tau * kLog2e;
+    const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
+    const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
+    const uint32_t ring_t = ring_base + 16u * ftid;
+    const uint32_t tm_t = tbase + tlane + tcol;
     uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
     for (int64_t t = cid; t < a.T; t += ncl) {
       if (__ldg(a.w_tok + t) == 0.f) continue;
@@ -256,56 +260,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       // online state with 4 independent partial sums (ILP), kept across chunks
-      float m2 = -INFINITY;
+      float m2 = 0.f;
       float s4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
       const uint32_t ts0 = ts;
-      uint4 v0, v1, n0 = make_uint4(0, 0, 0, 0), n1 = make_uint4(0, 0, 0, 0);
-      {
-        mbar_wait(smem_u32(&full_bar[slot]), ph);
-        const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
-        v0 = lds128(sa);
-        v1 = lds128(sa + kCB / 2);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
+      for (int k = 0; k < nck; ++k) {
+        mbar_wait(full0 + 8u * slot, ph);
+        const uint32_t sa = ring_t + slot * kCB;
+        uint4 v0 = lds128(sa);
+        uint4 v1 = lds128(sa + kCB / 2);
+        mbar_arrive(empty0 + 8u * slot);  // release semantics order the reads first
         if (++slot == kSlots) {
           slot = 0;
           ph ^= 1u;
         }
-      }
-      {
-        // base of the row's exponent arguments: this thread's max of chunk 0.
-        // Later elements may exceed it (arguments > 0 are fine); only a jump
-        // of > 126 in log2 units overflows, which the row-end repair handles.
-        float x[NE];
-        unpack(logits, v0, v1, x);
-        float xm = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < NE; ++j)
-          if (elem_off<T>(ftid, j) < slice_len) xm = fmaxf(xm, x[j]);
-        m2 = xm * c;
-        if (!(m2 > -INFINITY)) m2 = 0.f;  // nothing finite: any finite base works
-      }
-      for (int k = 0; k < nck; ++k) {
-        // opportunistic prefetch of the next chunk (only if it has already landed)
-        bool have_next = false;
-        if (k + 1 < nck && mbar_test(smem_u32(&full_bar[slot]), ph)) {
-          const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
-          n0 = lds128(sa);
-          n1 = lds128(sa + kCB / 2);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
-          if (++slot == kSlots) {
-            slot = 0;
-            ph ^= 1u;
-          }
-          have_next = true;
-        }
         // stash the raw words in TMEM for the backward warps
-        mbar_wait(smem_u32(&tempty_bar[ts]), tph ^ 1u);
+        mbar_wait(tempty0 + 8u * ts, tph ^ 1u);
         tc_fence_after();
-        tmem_st8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
+        tmem_st8(tm_t + ts * static_cast<uint32_t>(kSlotCols), v0, v1);
         float x[NE];
         unpack(logits, v0, v1, x);
+        if (k == 0) {
+          // base of the row's exponent arguments: this thread's max of chunk 0.
+          // Later elements may exceed it (arguments > 0 are fine); only a jump
+          // of > 126 in log2 units overflows, which the row-end repair handles.
+          float xm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            if (elem_off<T>(ftid, j) < slice_len) xm = fmaxf(xm, x[j]);
+          m2 = xm * c;
+          if (!(m2 > -INFINITY)) m2 = 0.f;  // nothing finite: any finite base works
+        }
         if (k == ck) {
 #pragma unroll
           for (int j = 0; j < NE; ++j)
@@ -334,26 +318,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_st(v0, v1);
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tfull_bar[ts]));
+        mbar_arrive(tfull0 + 8u * ts);
         if (++ts == kTSlots) {
           ts = 0;
           tph ^= 1u;
         }
-        if (k + 1 < nck && !have_next) {
-          mbar_wait(smem_u32(&full_bar[slot]), ph);
-          const uint32_t sa = ring_base + slot * kCB + 16u * ftid;
-          n0 = lds128(sa);
-          n1 = lds128(sa + kCB / 2);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&empty_bar[slot]));
-          if (++slot == kSlots) {
-            slot = 0;
-            ph ^= 1u;
-          }
-        }
-        v0 = n0;
-        v1 = n1;
       }
       Stats my{m2, (s4[0] + s4[1]) + (s4[2] + s4[3]), (w4[0] + w4[1]) + (w4[2] + w4[3])};
       // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
@@ -365,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t q = ts0;
         for (int k = 0; k < nck; ++k) {
           uint4 v0r, v1r;
-          tmem_ld8(tbase + tlane + q * static_cast<uint32_t>(kSlotCols) + tcol, v0r, v1r);
+          tmem_ld8(tm_t + q * static_cast<uint32_t>(kSlotCols), v0r, v1r);
           tmem_wait_ld(v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
@@ -380,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         q = ts0;
         for (int k = 0; k < nck; ++k) {
           uint4 v0r, v1r;
-          tmem_ld8(tbase + tlane + q * static_cast<uint32_t>(kSlotCols) + tcol, v0r, v1r);
+          tmem_ld8(tm_t + q * static_cast<uint32_t>(kSlotCols), v0r, v1r);
           tmem_wait_ld(v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
@@ -440,6 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float c = a.inv_tau * kLog2e;
     const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
     const bool leader = (crank == 0 && btid == 0);
+    const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
+    const uint32_t tm_t = tbase + tlane + tcol;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t ts = 0, tph = 0, nrow = 0;
     for (int64_t t = cid; t < a.T; t += ncl) {
@@ -504,45 +475,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
       const uint32_t sgn = neg ? 0x80008000u : 0u;
       const float gts = neg ? -gt : gt;  // target term before the sign flip
-      uint4 v0, v1;
-      uint32_t cur = ts;
-      mbar_wait(smem_u32(&tfull_bar[ts]), tph);
-      tc_fence_after();
-      tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
-      if (++ts == kTSlots) {
-        ts = 0;
-        tph ^= 1u;
-      }
-      bool pending = true;  // a TMEM load for chunk k is in flight
       for (int k = 0; k < nck; ++k) {
-        if (!pending) {
-          mbar_wait(smem_u32(&tfull_bar[ts]), tph);
-          tc_fence_after();
-          tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
-          cur = ts;
-          if (++ts == kTSlots) {
-            ts = 0;
-            tph ^= 1u;
-          }
-        }
-        tmem_wait_ld(v0, v1);
+        mbar_wait(tfull0 + 8u * ts, tph);
+        tc_fence_after();
+        uint4 w0, w1;
+        tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
+        tmem_wait_ld(w0, w1);
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[cur]));
-        const uint4 w0 = v0, w1 = v1;
-        bool have_next = false;
-        if (k + 1 < nck && mbar_test(smem_u32(&tfull_bar[ts]), tph)) {
-          // next chunk already stashed: start its TMEM load before computing this one
-          tc_fence_after();
-          tmem_ld8(tbase + tlane + ts * static_cast<uint32_t>(kSlotCols) + tcol, v0, v1);
-          cur = ts;
-          if (++ts == kTSlots) {
-            ts = 0;
-            tph ^= 1u;
-          }
-          have_next = true;
+        mbar_arrive(tempty0 + 8u * ts);
+        if (++ts == kTSlots) {
+          ts = 0;
+          tph ^= 1u;
         }
-        pending = have_next;
         float x[NE], gr[NE];
         unpack(logits, w0, w1, x);
         T* dst = drow + k * CE;
