@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // online state with 4 independent partial sums (ILP), kept across chunks
       float m2 = 0.f;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f}, w4[4] = {0.f, 0.f, 0.f, 0.f};
+      // two float2 partial sums = 4 independent chains, updated with FADD2/FFMA2
+      float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t ts0 = ts;
       for (int k = 0; k < nck; ++k) {
         mbar_wait(full0 + 8u * slot, ph);
@@ -296,12 +298,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == jt) zyv[nrow & 1] = x[j] * a.inv_tau;
         }
         if (k < nfull) {
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
 #pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const float av = fmaf(x[j], c, -m2);
-            const float e = ex2(av);
-            s4[j & 3] += e;
-            w4[j & 3] = fmaf(e, av, w4[j & 3]);
+          for (int p = 0; p < NE / 2; ++p) {
+            const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
+            const float2 e = make_float2(ex2(av.x), ex2(av.y));
+            s2[p & 1] = __fadd2_rn(s2[p & 1], e);
+            w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
           }
         } else {
           // last (partial) chunk of the slice: masked, -inf safe
@@ -311,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
               const float av = fmaf(x[j], c, -m2);
               const float e = ex2(av);
-              s4[0] += e;
-              w4[0] = fmaf(e, av, w4[0]);
+              s2[0].x += e;
+              w2[0].x = fmaf(e, av, w2[0].x);
             }
           }
         }
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
       }
-      Stats my{m2, (s4[0] + s4[1]) + (s4[2] + s4[3]), (w4[0] + w4[1]) + (w4[2] + w4[3])};
+      Stats my{m2, (s2[0].x + s2[1].x) + (s2[0].y + s2[1].y), (w2[0].x + w2[1].x) + (w2[0].y + w2[1].y)};
       // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
       // (a logit > 126/log2e above the chunk-0 base) made s or w non-finite:
       // recompute this thread's partials exactly from its TMEM words.
@@ -493,8 +496,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = k < nfull;
         if (G::es == 2 && c1 == 0.f) {
           // bf16: |c0| folded into the exponent, sign applied on the packed words
+          const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2f, -lse2f);
 #pragma unroll
-          for (int j = 0; j < NE; ++j) gr[j] = ex2(fmaf(x[j], c, -lse2f));
+          for (int p = 0; p < NE / 2; ++p) {
+            const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+            gr[2 * p] = ex2(av.x);
+            gr[2 * p + 1] = ex2(av.y);
+          }
           if (k == ck) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
@@ -517,8 +525,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < NE; ++j) gr[j] = neg ? -gr[j] : gr[j];
         } else if (c1 == 0.f) {
+          const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2, -lse2);
+          const float2 mc0 = make_float2(-c0, -c0);
 #pragma unroll
-          for (int j = 0; j < NE; ++j) gr[j] = -ex2(fmaf(x[j], c, -lse2)) * c0;
+          for (int p = 0; p < NE / 2; ++p) {
+            const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+            const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), mc0);
+            gr[2 * p] = g2.x;
+            gr[2 * p + 1] = g2.y;
+          }
           if (k == ck) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
