@@ -1,0 +1,64 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Vocab-parallel fused loss (SURVEY.md §8 row a7, §8e partitioning B).
+
+Rank p of P holds logits[:, vs_p : vs_p + Vp] (the natural output of a
+vocab-parallel LM head). One step is:
+
+  1. sf_tm_vp_partial_stats on the local shard -> stats[T, 4] =
+     {max z, sum e^(z - max), sum e^(z - max)(z - max), z_target or NaN};
+  2. all_gather of stats over the group (NCCL over NVLink; 16 B/token/rank,
+     versus 4V/P B/token of HBM traffic per rank);
+  3. sf_tm_vp_loss_fwd_bwd: every rank merges the P partials in rank order
+     (identical lse/entropy/logp/loss on every rank) and writes its shard's
+     dlogits.
+
+The exchange is a single collective (all_gather) instead of the MAX then SUM
+all-reduce pair; it carries the same information and lets every rank merge in
+the same fixed order, so the per-token scalars are bitwise identical across
+ranks. The reference has no counterpart (no NCCL anywhere; the
+paper's GPU-resident transport is PAPER.md:250,577).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import train_math as tm
+from ._lib import LossParams
+
+
+def shard_bounds(V: int, P: int, align: int = 8) -> list[int]:
+    """Vocab shard boundaries [b0=0, ..., bP=V] with every shard start aligned
+    to `align` elements (16 B for bf16) so each shard row can be TMA-streamed."""
+    if P < 1 or V < 1:
+        raise ValueError("need V >= 1 and P >= 1")
+    b = [((V * p) // P) // align * align for p in range(P)] + [V]
+    for i in range(P):
+        if b[i + 1] <= b[i]:
+            raise ValueError(f"vocab {V} too small for {P} aligned shards")
+    return b
+
+
+def gather_stats(local_stats: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather per-rank [T, 4] partial statistics into [P, T, 4] (rank order)."""
+    P = dist.get_world_size(group)
+    T = local_stats.shape[0]
+    out = torch.empty((P * T,) + tuple(local_stats.shape[1:]), dtype=local_stats.dtype, device=local_stats.device)
+    dist.all_gather_into_tensor(out, local_stats.contiguous(), group=group)
+    return out.view((P, T) + tuple(local_stats.shape[1:]))
+
+
+def vp_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
+                       params: Optional[LossParams] = None, dlogits=None, group=None, want_logp: bool = False,
+                       inv_temperature: Optional[float] = None):
+    """Fused DAPO/GRPO loss fwd+bwd on a vocab shard; returns
+    (metrics, dlogits_shard, logp, entropy) — metrics identical on every rank."""
+    if params is None:
+        params = tm.default_loss_params()
+    it = params.inv_temperature if inv_temperature is None else inv_temperature
+    stats = tm.vp_partial_stats(shard, targets, vocab_start, it)
+    gathered = gather_stats(stats, group)
+    return tm.vp_loss_fwd_bwd(shard, vocab_start, gathered, targets, old_logp, ref_logp, adv_tok, w_tok, params,
+                              dlogits=dlogits, want_logp=want_logp)

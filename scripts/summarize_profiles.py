@@ -1,0 +1,112 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Summarise a round's ncu evidence (gpurun_out/ev_*) into tracked files under
+profiles/ (run here, after scripts/prof_evidence.sh ran under gpurun).
+
+  python scripts/summarize_profiles.py r1
+"""
+import collections
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+
+def launches(tag):
+    src = os.path.join(OUT, "ev_launches.csv")
+    lines = [l for l in open(src) if not l.startswith("==")]
+    rows = list(csv.DictReader(io.StringIO("".join(lines))))
+    with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
+        f.write("".join(lines))
+    tot = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0]
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r["Metric Unit"]
+        ns = v * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1}.get(unit, 1)
+        tot[name] += ns
+        cnt[name] += 1
+    allns = sum(tot.values())
+    md = [f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 1`",
+          "", "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400` (cold-cache, serialised: compare shares).",
+          "", "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        md.append(f"| `{k}` | {cnt[k]} | {v / 1e6:.3f} | {v / allns * 100:.2f}% |")
+    return "\n".join(md)
+
+
+def ncu_raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    return {h: (u, v) for h, u, v in zip(r[0], r[1], r[2])}
+
+
+def full(tag):
+    rep = os.path.join(OUT, "ev_full.ncu-rep")
+    shutil.copy(rep, os.path.join(PROF, f"{tag}_fused_full.ncu-rep"))
+    raw = ncu_raw(rep)
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+            "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
+            "smsp__warps_active.avg.per_cycle_active"]
+    md = [f"# {tag}: `ncu --set full` of the fused loss kernel (`loss_tmem_kernel<bf16, C=2>`)", "",
+          "Command: `python bench.py --seqs-per-mb 4 --micro-batches 1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline`",
+          "(16,384 rows x V=151,936 bf16; one launch captured after warm-up). Report: "
+          f"`profiles/{tag}_fused_full.ncu-rep`.", "", "| metric | value |", "|---|---|"]
+    for k in keys:
+        if k in raw:
+            u, v = raw[k]
+            md.append(f"| `{k}` | {v} {u} |")
+    stalls = {k: raw[k][1] for k in raw if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")}
+    md += ["", "Stall reasons (warps per issued instruction):", "", "| reason | ratio |", "|---|---|"]
+    for k, v in sorted(stalls.items(), key=lambda kv: -float(kv[1] or 0))[:10]:
+        md.append(f"| {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} | {v} |")
+    return "\n".join(md)
+
+
+def traffic(tag):
+    lines = [l for l in open(os.path.join(OUT, "ev_traffic.csv")) if not l.startswith("==")]
+    rows = list(csv.DictReader(io.StringIO("".join(lines))))
+    vals = {r["Metric Name"]: float(r["Metric Value"].replace(",", "")) for r in rows}
+    rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
+    j = {"kernel": "loss_tmem_kernel<bf16,C=2>", "vocab": 151936, "rows": 131072,
+         "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+         "ncu_duration_ns": vals.get("gpu__time_duration.sum"),
+         "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+                    "-k regex:loss_tmem_kernelItLi2E -s 2 -c 1 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline",
+         "round": tag}
+    json.dump(j, open(os.path.join(PROF, "fused_loss_traffic.json"), "w"), indent=1)
+    return j
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    os.makedirs(PROF, exist_ok=True)
+    parts = [launches(tag), "", full(tag)]
+    t = traffic(tag)
+    parts += ["", f"# {tag}: DRAM traffic of one headline launch (131,072 rows x 151,936 bf16)", "",
+              f"read {t['dram_bytes_read'] / 1e9:.3f} GB + write {t['dram_bytes_write'] / 1e9:.3f} GB = "
+              f"{t['dram_bytes_per_launch'] / 1e9:.3f} GB per launch (ncu duration {t['ncu_duration_ns'] / 1e6:.3f} ms)."]
+    bench = [l for l in open(os.path.join(OUT, "ev_plain.log")) if l.startswith("{")]
+    if bench:
+        d = json.loads(bench[-1])
+        json.dump(d, open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
+        parts += ["", f"# {tag}: bench line of the same run (not under ncu)", "", "```", json.dumps(d, indent=1), "```"]
+    open(os.path.join(PROF, f"{tag}_summary.md"), "w").write("\n".join(parts) + "\n")
+    print("\n".join(parts))
+
+
+if __name__ == "__main__":
+    main()
