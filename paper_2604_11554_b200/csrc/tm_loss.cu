@@ -47,7 +47,8 @@ constexpr int kFW = 12;                     // forward warps (3 per SM sub-parti
 constexpr int kBW = 12;                     // backward warps (3 per SM sub-partition)
 constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
-constexpr int kThreads = (kFW + kBW + 1) * 32;  // 800
+constexpr int kCtl = kFW + kBW + 1;         // control warp: row merge, cluster exchange, scalars
+constexpr int kThreads = (kFW + kBW + 2) * 32;  // 832
 constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per thread = 12 KB
 constexpr int kSlots = 17;                  // smem ring slots (204 KB)
 constexpr int kRingBytes = kSlots * kCB;
@@ -55,6 +56,15 @@ constexpr int kSlotCols = kCB / (128 * 4);  // TMEM columns per chunk slot (24)
 constexpr int kTSlots = 512 / kSlotCols;    // 21 TMEM chunk slots (252 KB)
 constexpr int kTCols = 512;
 constexpr int kMailD = 8;                   // mailbox ring depth (rows)
+constexpr int kRD = 4;                      // depth of the per-row partial / scalar rings
+
+// Per-row scalars computed once by the control warp and broadcast in smem.
+struct RowScal {
+  float lse2, lse2f, c0, c1, gt;
+  int yl;          // target column relative to this CTA's slice (or out of range)
+  uint32_t sgn;    // 0x80008000 when dlogits entries are -p*|c0| (bf16 fast path)
+  float pad;
+};
 constexpr int kMaxChunks = 14;              // row-slice chunks that keep >= 7 TMEM slots free
 
 template <typename T>
@@ -169,8 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t tempty_bar[kTSlots];
   __shared__ __align__(8) uint64_t mail_bar[kMailD];
   __shared__ __align__(16) float4 mail[kMailD][8];
-  __shared__ __align__(16) float4 red[2][kFW];
-  __shared__ float zyv[2];
+  __shared__ __align__(16) float4 red[kRD][kFW];      // per forward warp: (m2, s, w, z_target|NaN)
+  __shared__ __align__(8) uint64_t red_bar[kRD];
+  __shared__ __align__(16) RowScal scal[kRD];
+  __shared__ __align__(8) uint64_t scal_bar[kRD];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x;
@@ -198,7 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&tempty_bar[i]), kFT);  // backward threads (same count)
     }
     for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
-    zyv[0] = zyv[1] = __int_as_float(0x7fc00000);
+    for (int i = 0; i < kRD; ++i) {
+      mbar_init(smem_u32(&red_bar[i]), kFW);  // lane 0 of each forward warp
+      mbar_init(smem_u32(&scal_bar[i]), 1);   // the control warp lane 0
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(smem_u32(&tmem_base_sh), kTCols);
@@ -265,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t ts0 = ts;
+      float zyt = __int_as_float(0x7fc00000);
       for (int k = 0; k < nck; ++k) {
         mbar_wait(full0 + 8u * slot, ph);
         const uint32_t sa = ring_t + slot * kCB;
@@ -295,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (k == ck) {
 #pragma unroll
           for (int j = 0; j < NE; ++j)
-            if (j == jt) zyv[nrow & 1] = x[j] * a.inv_tau;
+            if (j == jt) zyt = x[j] * a.inv_tau;
         }
         if (k < nfull) {
           const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
@@ -371,70 +387,74 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (bad) my = Stats{mb2, sr, wr};
       }
       if (my.s == 0.f) my = stats_empty();  // nothing finite in this thread's share
-      // CTA reduction of the forward partials, then DSMEM mailbox broadcast.
+      // Per-warp partial -> smem ring; no CTA barrier: the control warp
+      // merges the 12 partials, so forward warps go straight to the next row.
       my = warp_merge(my);
-      const uint32_t b2 = nrow & 1u;
-      if (lane == 0) red[b2][warp] = make_float4(my.m2, my.s, my.w, 0.f);
-      named_bar_sync(1, kFT);
-      if (warp == 0) {
-        Stats v = stats_empty();
-        if (lane < kFW) {
-          const float4 r = red[b2][lane];
-          v = Stats{r.x, r.y, r.z};
-        }
-        v = warp_merge(v);
-        if (lane == 0) {
-          const float z = zyv[b2];
-          zyv[b2] = __int_as_float(0x7fc00000);
-          const uint32_t mb = nrow % kMailD;
-          if (C == 1) {
-            mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
-            mbar_arrive(smem_u32(&mail_bar[mb]));
-          } else {
-            const uint32_t my_slot = smem_u32(&mail[mb][crank]);
-            const uint32_t my_bar = smem_u32(&mail_bar[mb]);
 #pragma unroll
-            for (int q = 0; q < C; ++q) {
-              st_cluster_v4(mapa(my_slot, q), v.m2, v.s, v.w, z);
-              mbar_arrive_remote(mapa(my_bar, q));
-            }
-          }
-        }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float oz = __shfl_xor_sync(0xffffffffu, zyt, o);
+        zyt = (zyt != zyt) ? oz : zyt;
+      }
+      if (lane == 0) {
+        red[nrow % kRD][warp] = make_float4(my.m2, my.s, my.w, zyt);
+        mbar_arrive(smem_u32(&red_bar[nrow % kRD]));
       }
       ++nrow;
     }
-  } else {
-    // ================================================================ backward
-    const int btid = tid - kFT;               // same element mapping as forward warp (warp-8)
-    const int fw = warp - kFW;
-    const uint32_t tlane = static_cast<uint32_t>(32 * (fw & 3)) << 16;
-    const uint32_t tcol = 8u * static_cast<uint32_t>(fw >> 2);
-    const float c = a.inv_tau * kLog2e;
+  } else if (warp == kCtl) {
+    // ================================================================ control
+    // Per row: merge the 12 forward partials, exchange with the cluster through
+    // DSMEM mailboxes, compute the loss scalars once and publish them to the
+    // backward warps. Never touches the row data, so it runs as far ahead as
+    // the forward warps allow.
     const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
-    const bool leader = (crank == 0 && btid == 0);
-    const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
-    const uint32_t tm_t = tbase + tlane + tcol;
+    const bool leader = (crank == 0 && lane == 0);
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t ts = 0, tph = 0, nrow = 0;
+    uint32_t nrow = 0;
     for (int64_t t = cid; t < a.T; t += ncl) {
       const float w = __ldg(a.w_tok + t);
       if (w == 0.f) {
-        if (!a.masked_skip) {
-          uint8_t* drow = reinterpret_cast<uint8_t*>(static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start);
-          const int nb = slice_len * G::es;
-          for (int off = btid * 16; off < nb; off += kFT * 16) stg128_cs(drow + off, make_uint4(0, 0, 0, 0));
-        }
         if (leader) {
           if (a.out_logp) a.out_logp[t] = 0.f;
           if (a.out_entropy) a.out_entropy[t] = 0.f;
         }
         continue;
       }
+      const uint32_t rs = nrow % kRD;
+      const uint32_t rpar = (nrow / kRD) & 1u;
       const float A = __ldg(a.adv_tok + t);
       const float old = __ldg(a.old_logp + t);
       const float ref = __ldg(a.ref_logp + t);
-      const int64_t yl = static_cast<int64_t>(__ldg(a.targets + t)) - a.vocab_start - slice_start;
+      const int64_t yl64 = static_cast<int64_t>(__ldg(a.targets + t)) - a.vocab_start - slice_start;
+      mbar_wait(smem_u32(&red_bar[rs]), rpar);
+      Stats v = stats_empty();
+      float z = __int_as_float(0x7fc00000);
+      if (lane < kFW) {
+        const float4 r = red[rs][lane];
+        v = Stats{r.x, r.y, r.z};
+        z = r.w;
+      }
+      v = warp_merge(v);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float oz = __shfl_xor_sync(0xffffffffu, z, o);
+        z = (z != z) ? oz : z;
+      }
       const uint32_t mb = nrow % kMailD;
+      if (lane == 0) {
+        if (C == 1) {
+          mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
+          mbar_arrive(smem_u32(&mail_bar[mb]));
+        } else {
+          const uint32_t my_slot = smem_u32(&mail[mb][crank]);
+          const uint32_t my_bar = smem_u32(&mail_bar[mb]);
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            st_cluster_v4(mapa(my_slot, q), v.m2, v.s, v.w, z);
+            mbar_arrive_remote(mapa(my_bar, q));
+          }
+        }
+      }
       if (C == 1) {
         mbar_wait(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u);
       } else {
@@ -458,20 +478,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.out_logp) a.out_logp[t] = logp;
         if (a.out_entropy) a.out_entropy[t] = H;
       }
-      // dlogits_v = gt*[v==y] - p_v*(c0 + c1*a_v), a_v = (z_v - lse)*log2e, p_v = 2^a_v.
-      const float gt = a.inv_tau * g;
-      const float c0 = a.inv_tau * (g + gH * H);
-      const float c1 = a.inv_tau * gH * kLn2;
-      // Fast form (c1 == 0): p_v*c0 = sign(c0) * 2^(a_v + log2|c0|).
-      const float lse2f = lse2 - log2f(fabsf(c0));
-      const bool neg = c0 > 0.f;  // gradient entries are -p*c0
+      if (lane == 0) {
+        // dlogits_v = gt*[v==y] - p_v*(c0 + c1*a_v), a_v = (z_v - lse)*log2e, p_v = 2^a_v;
+        // fast form (c1 == 0): p_v*c0 = sign(c0) * 2^(a_v + log2|c0|).
+        RowScal r;
+        r.lse2 = lse2;
+        r.gt = a.inv_tau * g;
+        r.c0 = a.inv_tau * (g + gH * H);
+        r.c1 = a.inv_tau * gH * kLn2;
+        r.lse2f = lse2 - log2f(fabsf(r.c0));
+        r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
+        r.yl = (yl64 >= 0 && yl64 < slice_len) ? static_cast<int>(yl64) : -1;
+        r.pad = 0.f;
+        scal[rs] = r;
+        mbar_arrive(smem_u32(&scal_bar[rs]));
+      }
+    
+      ++nrow;
+    }
+    if (leader) finish_metrics(a, cid, ncl, acc);
+  } else {
+    // ================================================================ backward
+    const int btid = tid - kFT;               // same element mapping as forward warp (warp-8)
+    const int fw = warp - kFW;
+    const uint32_t tlane = static_cast<uint32_t>(32 * (fw & 3)) << 16;
+    const uint32_t tcol = 8u * static_cast<uint32_t>(fw >> 2);
+    const float c = a.inv_tau * kLog2e;
+    const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
+    const uint32_t tm_t = tbase + tlane + tcol;
+    uint32_t ts = 0, tph = 0, nrow = 0;
+    for (int64_t t = cid; t < a.T; t += ncl) {
+      const float w = __ldg(a.w_tok + t);
+      if (w == 0.f) {
+        if (!a.masked_skip) {
+          uint8_t* drow = reinterpret_cast<uint8_t*>(static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start);
+          const int nb = slice_len * G::es;
+          for (int off = btid * 16; off < nb; off += kFT * 16) stg128_cs(drow + off, make_uint4(0, 0, 0, 0));
+        }
+        continue;
+      }
+      const uint32_t rs = nrow % kRD;
+      const uint32_t rpar = (nrow / kRD) & 1u;
+      mbar_wait(smem_u32(&scal_bar[rs]), rpar);
+      const RowScal rsc = scal[rs];
+      const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
+      const bool neg = rsc.sgn != 0u;
       int ck = -1, jt = 0;
-      if (yl >= 0 && yl < slice_len) {
-        const int r = static_cast<int>(yl % CE);
+      if (rsc.yl >= 0) {
+        const int r = rsc.yl % CE;
         const int v = r >= G::HALF ? 1 : 0;
         const int rr = r - v * G::HALF;
         if (rr / EV == btid) {
-          ck = static_cast<int>(yl / CE);
+          ck = rsc.yl / CE;
           jt = v * EV + rr % EV;
         }
       }
@@ -565,7 +623,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++nrow;
     }
-    if (leader) finish_metrics(a, cid, ncl, acc);
   }
 
   // teardown: every TMEM access is complete before warp 0 frees it
