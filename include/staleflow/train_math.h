@@ -245,6 +245,12 @@ int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_
  * tests can cover both code paths; process-wide. Not for production use. */
 int sf_tm_debug_force_generic(int on);
 
+/* on a non-NULL device buffer of 16 uint64 (zeroed by the caller), the fused
+ * loss kernel accumulates per-role clock64 cycle sums: for role r in
+ * {producer, forward, control, backward}: [3r] active, [3r+1] and [3r+2] the
+ * two wait classes, [12+r] warp count. NULL turns it off. Debug/tuning only. */
+int sf_tm_debug_wait_counters(void* dev_counters);
+
 #ifdef __cplusplus
 }
 #endif

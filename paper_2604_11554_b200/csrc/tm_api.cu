@@ -581,9 +581,13 @@ int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_
   return check_cuda(h, e, "sf_tm_synth_logits");
 }
 
-// Test hook (not in the public header): route row kernels to the generic path.
 int sf_tm_debug_force_generic(int on) {
   sftm::set_force_generic(on != 0);
+  return SF_TM_OK;
+}
+
+int sf_tm_debug_wait_counters(void* dev_counters) {
+  sftm::set_debug_counters(static_cast<unsigned long long*>(dev_counters));
   return SF_TM_OK;
 }
 

@@ -41,6 +41,8 @@ struct RowArgs {
   const float* gathered = nullptr;  // VpBwd: [P,T,4]
   int P = 1;
   float* out_metrics = nullptr;
+  // optional wait-time instrumentation (debug only): per-role clock64 sums
+  unsigned long long* dbg = nullptr;
   // workspace (owned by the handle)
   double* partials = nullptr;  // [max_blocks * 8]
   unsigned* ticket = nullptr;
@@ -60,6 +62,11 @@ int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, La
 
 // Forces the generic (non-TMA) kernel; used by tests to cover both paths.
 void set_force_generic(bool on);
+// Debug: device buffer of kDbgCounters u64 that the fused loss kernel fills with
+// per-role busy/wait cycle sums (nullptr = off).
+constexpr int kDbgCounters = 16;
+void set_debug_counters(unsigned long long* dev_ptr);
+unsigned long long* debug_counters();
 
 int launch_varlen_meta(const int32_t* seq_lens, const int32_t* prompt_lens,
                        const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,

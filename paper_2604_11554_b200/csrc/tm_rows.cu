@@ -30,6 +30,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(kGT) rows_generic_kernel(const RowArgs a) {
 // ===========================================================================
 // Host-side launch logic.
 // ===========================================================================
-int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info);  // tm_loss.cu
+int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info);  // tm_loss.cu (v2 schedule)
+int launch_loss_v3(const RowArgs& a, cudaStream_t s, LaunchInfo* info);    // tm_loss3.cu (v3 schedule)
 
 namespace {
 
@@ -550,7 +552,13 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
 
   if (ring_ok) {
     if (mode == kModeFwdBwd) {
-      const int e = launch_loss_tmem(a, s, info);
+      // default: role-split schedule (tm_loss.cu); SFTM_LOSS_VARIANT=3 selects the
+      // per-warp software-pipelined schedule (tm_loss3.cu) for A/B comparisons
+      static const int variant = [] {
+        const char* v = getenv("SFTM_LOSS_VARIANT");
+        return (v && v[0] == '3') ? 3 : 2;
+      }();
+      const int e = variant == 2 ? launch_loss_tmem(a, s, info) : launch_loss_v3(a, s, info);
       if (e != -2) return e;  // -2: slice too wide for TMEM residency -> generic
     } else {
       const int nslots = kStreamRingBytes / CB;
@@ -577,6 +585,12 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
 }  // namespace
 
 void set_force_generic(bool on) { g_force_generic = on; }
+
+namespace {
+unsigned long long* g_dbg = nullptr;
+}
+void set_debug_counters(unsigned long long* p) { g_dbg = p; }
+unsigned long long* debug_counters() { return g_dbg; }
 
 int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, LaunchInfo* info) {
   if (a.dtype == 1) return dispatch<uint16_t>(a, mode, s, err, info);
