@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     ap.add_argument("--generic", action="store_true", help="force the generic two-pass kernel (comparison)")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (1-based); 2 = the headline (default)")
     return ap.parse_args()
 
 
@@ -226,6 +228,19 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.config != 2:
+        import bench_extra
+
+        if args.config in (1, 4):
+            bench_extra.run_loss_config(args, args.config, world, rank, dev, dist)
+        elif args.config == 3:
+            bench_extra.run_r3(args, world, rank, dev, dist)
+        else:
+            bench_extra.run_vocab_parallel(args, world, rank, dev, dist)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     h = tm.handle(local)
     V, L, S, M, G = args.vocab, args.seq_len, args.seqs_per_mb, args.micro_batches, args.group
     n_seq = S * M
