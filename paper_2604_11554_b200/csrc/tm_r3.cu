@@ -232,6 +232,234 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fast path (E % 64 == 0, E <= 256, k <= 16): 16-lane groups, two rows per warp
+// instruction. Lane l of a group owns experts {i*64 + 4l + c : c < 4} for
+// i < E/64 (two float4 loads per 64 experts -> fully coalesced rows).
+// The trainer top-k set equals the recorded set iff the best non-recorded expert
+// ranks below the worst recorded one under the order (logit desc, index asc):
+// one min and one max reduction (plus an index tie-break only on equal logits)
+// instead of k argmax rounds.
+// ---------------------------------------------------------------------------
+constexpr unsigned kG = 16;  // lanes per row group
+
+__device__ __forceinline__ float gmaxf(float v) {
+#pragma unroll
+  for (int o = kG / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, kG));
+  return v;
+}
+__device__ __forceinline__ float gsumf(float v) {
+#pragma unroll
+  for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, kG);
+  return v;
+}
+__device__ __forceinline__ int gsumi(int v) {
+#pragma unroll
+  for (int o = kG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, kG);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void r3_load4(const T* p, float (&z)[4]);
+template <>
+__device__ __forceinline__ void r3_load4<float>(const float* p, float (&z)[4]) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  z[0] = v.x; z[1] = v.y; z[2] = v.z; z[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void r3_load4<uint16_t>(const uint16_t* p, float (&z)[4]) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  z[0] = bf16lo(v.x); z[1] = bf16hi(v.x); z[2] = bf16lo(v.y); z[3] = bf16hi(v.y);
+}
+
+template <typename T, int NB>  // NB = E / 64 blocks of 64 experts
+__global__ void __launch_bounds__(256)
+    r3_fwd_fast(const T* __restrict__ logits, int64_t L, int64_t Tn, int k, const void* __restrict__ rec,
+                int idx_dtype, int renorm, float* __restrict__ out_w, int32_t* __restrict__ out_idx,
+                uint32_t* __restrict__ mismatch) {
+  constexpr int E = NB * 64;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (kG - 1);            // lane within the row group
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t rows = L * Tn;
+  const int64_t pairs = (rows + 1) / 2;
+  const int64_t per = (pairs + nw - 1) / nw;  // contiguous pair range per warp
+  int64_t p0 = gw * per, p1 = p0 + per;
+  if (p1 > pairs) p1 = pairs;
+  int64_t cur_layer = 0, layer_end = -1;  // forces a (single) division on the first row
+  uint32_t cur_cnt = 0;
+  // rows of the next pair are loaded one iteration ahead (two pairs in flight per warp)
+  float zn[NB][4];
+  if (p0 < p1) {
+    const int64_t r = 2 * p0 + (lane >> 4);
+    const int64_t rc = r < rows ? r : rows - 1;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+  }
+  for (int64_t pr = p0; pr < p1; ++pr) {
+    const int64_t row = 2 * pr + (lane >> 4);
+    const bool valid = row < rows;
+    const int64_t rowc = valid ? row : rows - 1;
+    float z[NB][4];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) z[i][c] = zn[i][c];
+    if (pr + 1 < p1) {
+      const int64_t r = 2 * (pr + 1) + (lane >> 4);
+      const int64_t rc = r < rows ? r : rows - 1;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+    }
+    int my_e = -1;
+    float zr = -INFINITY;
+    if (gl < k) {
+      my_e = r3_idx(rec, idx_dtype, rowc * k + gl);
+      zr = (my_e >= 0 && my_e < E) ? r3_load(logits, rowc * E + my_e) : __int_as_float(0x7fc00000);
+    }
+    // membership of my experts in the recorded set (k <= 16, unrolled)
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < k) {
+        const int e = __shfl_sync(0xffffffffu, my_e, j, kG);
+        if (e >= 0 && e < E && ((e & 63) >> 2) == gl) mine |= 1u << ((e >> 6) * 4 + (e & 3));
+      }
+    }
+    // gate weights
+    float wj;
+    if (renorm) {
+      const float mx = gmaxf(gl < k ? zr : -INFINITY);
+      const float ez = gl < k ? __expf(zr - mx) : 0.f;
+      wj = __fdividef(ez, gsumf(ez));
+    } else {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mx = fmaxf(mx, z[i][c]);
+      mx = gmaxf(mx);
+      float se = 0.f;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) se += __expf(z[i][c] - mx);
+      wj = __fdividef(__expf(zr - mx), gsumf(se));
+    }
+    if (valid && gl < k) {
+      out_w[row * k + gl] = wj;
+      if (out_idx) out_idx[row * k + gl] = my_e;
+    }
+    if (mismatch) {
+      // worst recorded vs best non-recorded logit; exact index tie-break (P9) only on equality
+      float in_min = INFINITY, out_max = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const bool rin = (mine >> (i * 4 + c)) & 1u;
+          in_min = rin ? fminf(in_min, z[i][c]) : in_min;
+          out_max = rin ? out_max : fmaxf(out_max, z[i][c]);
+        }
+#pragma unroll
+      for (int o = kG / 2; o > 0; o >>= 1) {
+        in_min = fminf(in_min, __shfl_xor_sync(0xffffffffu, in_min, o, kG));
+        out_max = fmaxf(out_max, __shfl_xor_sync(0xffffffffu, out_max, o, kG));
+      }
+      const int distinct = gsumi(__popc(mine));
+      bool mm = (distinct != k) || (out_max > in_min);
+      if (__any_sync(0xffffffffu, out_max == in_min)) {
+        // tie: the trainer prefers the lower index among equal logits
+        int in_hi = -1, out_lo = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int e = i * 64 + 4 * gl + c;
+            const bool rin = (mine >> (i * 4 + c)) & 1u;
+            if (rin && z[i][c] == in_min) in_hi = max(in_hi, e);
+            if (!rin && z[i][c] == out_max) out_lo = min(out_lo, e);
+          }
+#pragma unroll
+        for (int o = kG / 2; o > 0; o >>= 1) {
+          in_hi = max(in_hi, __shfl_xor_sync(0xffffffffu, in_hi, o, kG));
+          out_lo = min(out_lo, __shfl_xor_sync(0xffffffffu, out_lo, o, kG));
+        }
+        if (out_max == in_min && out_lo < in_hi) mm = true;
+      }
+      // per-layer counts; the layer boundary advances incrementally (no 64-bit division per row)
+      const unsigned bal = __ballot_sync(0xffffffffu, valid && mm && gl == 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t rr = 2 * pr + h;
+        if (rr >= rows) continue;
+        if (rr >= layer_end) {
+          if (cur_cnt && lane == 0) {
+            atomicAdd(mismatch + cur_layer, cur_cnt);
+            atomicAdd(mismatch + L, cur_cnt);
+          }
+          cur_layer = rr / Tn;
+          layer_end = (cur_layer + 1) * Tn;
+          cur_cnt = 0;
+        }
+        if ((bal >> (h * 16)) & 1u) ++cur_cnt;
+      }
+    }
+  }
+  if (mismatch && cur_cnt && lane == 0) {
+    atomicAdd(mismatch + cur_layer, cur_cnt);
+    atomicAdd(mismatch + L, cur_cnt);
+  }
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(256)
+    r3_bwd_fast(int64_t rows, int k, const void* __restrict__ rec, int idx_dtype, const float* __restrict__ w,
+                const float* __restrict__ dw, T* __restrict__ dz) {
+  constexpr int E = NB * 64;
+  __shared__ __align__(16) float buf[8][2][E];  // per warp: the two rows of a pair
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (kG - 1);
+  const int half = lane >> 4;
+  float* rb = buf[threadIdx.x >> 5][half];
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t pr = gw; 2 * pr < rows; pr += nw) {
+    const int64_t row = 2 * pr + half;
+    const bool valid = row < rows;
+    const int64_t rowc = valid ? row : rows - 1;
+    int my_e = -1;
+    float wj = 0.f, dwj = 0.f;
+    if (gl < k) {
+      my_e = r3_idx(rec, idx_dtype, rowc * k + gl);
+      wj = w[rowc * k + gl];
+      dwj = dw[rowc * k + gl];
+    }
+    const float S = gsumf(wj * dwj);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) *reinterpret_cast<float4*>(rb + i * 64 + 4 * gl) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    // dz[e_j] += w_j (dw_j - S); duplicates of a recorded expert accumulate
+    if (gl < k && my_e >= 0 && my_e < E) atomicAdd(rb + my_e, wj * (dwj - S));
+    __syncwarp();
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const float4 o = *reinterpret_cast<const float4*>(rb + i * 64 + 4 * gl);
+        T* d = dz + row * E + i * 64 + 4 * gl;
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<float4*>(d) = o;
+        } else {
+          *reinterpret_cast<uint2*>(d) = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 namespace {
 int r3_grid(int64_t rows) {
   int dev = 0, sms = 148;
@@ -251,6 +479,27 @@ int r3_grid(int64_t rows) {
 int launch_r3_fwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
                   const void* rec_idx, int idx_dtype, int renorm, float* out_w, int32_t* out_idx,
                   uint32_t* out_mismatch, cudaStream_t s, int* launches) {
+  if (E % 64 == 0 && E <= 256 && k <= 16) {
+    const int grid = r3_grid((L * T + 1) / 2);
+#define LAUNCH_FF(NB)                                                                                  \
+  if (dtype == 1)                                                                                      \
+    r3_fwd_fast<uint16_t, NB><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(logits), L, T,         \
+                                                   static_cast<int>(k), rec_idx, idx_dtype, renorm,    \
+                                                   out_w, out_idx, out_mismatch);                      \
+  else                                                                                                 \
+    r3_fwd_fast<float, NB><<<grid, 256, 0, s>>>(static_cast<const float*>(logits), L, T,               \
+                                                static_cast<int>(k), rec_idx, idx_dtype, renorm, out_w, \
+                                                out_idx, out_mismatch);
+    switch (E / 64) {
+      case 1: LAUNCH_FF(1) break;
+      case 2: LAUNCH_FF(2) break;
+      case 3: LAUNCH_FF(3) break;
+      default: LAUNCH_FF(4) break;
+    }
+#undef LAUNCH_FF
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const int grid = r3_grid(L * T);
 #define LAUNCH_F(NPL)                                                                           \
   (dtype == 1 ? (r3_fwd_kernel<uint16_t, NPL><<<grid, 256, 0, s>>>(                             \
@@ -273,6 +522,25 @@ int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E
                   const void* rec_idx, int idx_dtype, int renorm, const float* w, const float* dw,
                   void* dlogits, cudaStream_t s, int* launches) {
   const int64_t rows = L * T;
+  if (renorm && E % 64 == 0 && E <= 256 && k <= 16) {
+    const int g2 = r3_grid((rows + 1) / 2);
+#define LAUNCH_BF(NB)                                                                                  \
+  if (dtype == 1)                                                                                      \
+    r3_bwd_fast<uint16_t, NB><<<g2, 256, 0, s>>>(rows, static_cast<int>(k), rec_idx, idx_dtype, w, dw, \
+                                                 static_cast<uint16_t*>(dlogits));                     \
+  else                                                                                                 \
+    r3_bwd_fast<float, NB><<<g2, 256, 0, s>>>(rows, static_cast<int>(k), rec_idx, idx_dtype, w, dw,    \
+                                              static_cast<float*>(dlogits));
+    switch (E / 64) {
+      case 1: LAUNCH_BF(1) break;
+      case 2: LAUNCH_BF(2) break;
+      case 3: LAUNCH_BF(3) break;
+      default: LAUNCH_BF(4) break;
+    }
+#undef LAUNCH_BF
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const int grid = r3_grid(rows);
 #define LAUNCH_B(NPL)                                                                           \
   (dtype == 1 ? (r3_bwd_kernel<uint16_t, NPL><<<grid, 256, 0, s>>>(                             \
