@@ -1,0 +1,81 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Multi-GPU (skipped with fewer than 2 GPUs): vocab-parallel fused loss over
+NCCL (one process per GPU) must reproduce the single-GPU fused kernel — same
+per-token logp/entropy on every rank, identical metrics on every rank, and the
+concatenated shard gradients equal to the unsharded dlogits."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        from paper_2604_11554_b200 import train_math as tm
+        from paper_2604_11554_b200.vocab_parallel import shard_bounds, vp_pg_loss_fwd_bwd
+
+        T, V = 96, 151936
+        g = torch.Generator(device="cpu").manual_seed(123)
+        logits = (torch.randn(T, V, generator=g) * 2).to(torch.bfloat16).to(dev)
+        targets = torch.randint(0, V, (T,), generator=g, dtype=torch.int32).to(dev)
+        lp, _, _ = tm.logprob_fwd(logits, targets)
+        old = (lp + 0.05 * torch.randn(T, generator=g).to(dev)).float()
+        ref = (lp + 0.1 * torch.randn(T, generator=g).to(dev)).float()
+        adv = torch.randn(T, generator=g).to(dev)
+        w = (torch.rand(T, generator=g) < 0.9).float().to(dev) / T
+        met_f, dl_f, lp_f, ent_f = tm.pg_loss_fwd_bwd(logits, targets, old, ref, adv, w, want_logp=True)
+        b = shard_bounds(V, world)
+        shard = logits[:, b[rank]:b[rank + 1]].contiguous()
+        met, dsh, lpv, entv = vp_pg_loss_fwd_bwd(shard, b[rank], targets, old, ref, adv, w, want_logp=True)
+        torch.cuda.synchronize()
+        ok_lp = torch.allclose(lpv, lp_f, atol=2e-6, rtol=2e-6)
+        ok_ent = torch.allclose(entv, ent_f, atol=2e-5, rtol=2e-5)
+        ref_sh = dl_f[:, b[rank]:b[rank + 1]].float()
+        diff = (dsh.float() - ref_sh).abs()
+        ok_dl = bool((diff <= ref_sh.abs() * 2 ** -7 + 1e-7).float().mean() > 0.9999)
+        allm = [torch.empty_like(met) for _ in range(world)]
+        dist.all_gather(allm, met)
+        ok_same = all(torch.equal(m, allm[0]) for m in allm)
+        ok_met = torch.allclose(met[:6], met_f[:6], atol=2e-6, rtol=2e-5)
+        q.put((rank, bool(ok_lp), bool(ok_ent), ok_dl, ok_same, bool(ok_met)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_vocab_parallel_nccl_matches_single_gpu():
+    import torch.multiprocessing as mp
+
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert all(r[1:]), r
