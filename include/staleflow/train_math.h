@@ -229,6 +229,12 @@ int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, in
                           const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
                           float* out_metrics, float* out_logp, float* out_entropy, void* stream);
 
+/* ---- pinned host staging (for the C++ seam adapter) ----------------------
+ * Page-locked host memory so the seam's H2D copies are asynchronous DMA.
+ * Returns ConfigError for bytes == 0 or out == NULL, Internal on CUDA errors. */
+int sf_tm_host_alloc(size_t bytes, void** out);
+int sf_tm_host_free(void* p);
+
 /* ---- synthetic inputs (bench / tests) ------------------------------------
  * Counter-based, seeded with the reference's SplitMix64 (rng.hpp:17-39)
  * evaluated at element index: u_i = mix64(seed + (i+1)*0x9e3779b97f4a7c15),

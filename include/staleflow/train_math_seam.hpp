@@ -1,0 +1,182 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// C++ trainer-seam adapter over the train-math C-ABI (staleflow/train_math.h).
+//
+// It turns one trainer MicroBatch, as delivered by the reference's bus
+// (proj/include/staleflow/types.hpp:48-59, StreamLoader::next_micro_batch,
+// stream_loader.cpp:77-91), into one fused loss fwd+bwd on the device-resident
+// LM-head logits. This is the drop-in for the latency stub at
+// proj/src/sim_runtime.cpp:441 / proj/src/wall_runtime.cpp:197.
+//
+// Header-only and templated on the MicroBatch type, so it compiles against the
+// reference's own staleflow::MicroBatch without changing proj/include. Required
+// members: field_set (sorted std::vector<std::string>), sample_ids, and
+// payloads[i][j] (bytes of field_set[j] for sample i).
+//
+// Field codecs (little-endian, SURVEY.md §8b "Payload / ownership"):
+//   response   int32[L_i]    token ids; logits row j scores response[j]
+//   logp       float32[L_i]  behaviour-policy log-probs (ActorFwd)
+//   ref_logp   float32[L_i]  reference-model log-probs (RefLogP)
+//   advantage  float32       per-sample GRPO advantage (Advantages stage)
+//   reward     float32       per-sample reward (used when there is no advantage
+//                            field: GRPO is then computed here over `group`)
+//   loss_mask  uint8[L_i]    optional; default all ones
+//   group      int32         optional group id; default (sample_id-1)/group_size
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "staleflow/train_math.h"
+
+namespace staleflow {
+namespace train_math {
+
+// Host arrays of one packed micro-batch (samples concatenated in bus order).
+struct PackedBatch {
+  int64_t T = 0, B = 0;
+  std::vector<int32_t> targets;
+  std::vector<float> logp, ref_logp;
+  std::vector<uint8_t> mask;
+  bool has_mask = false;
+  std::vector<int32_t> seq_lens, group_ids;
+  std::vector<float> per_sample;  // advantages, or rewards when !has_advantage
+  bool has_advantage = false;
+};
+
+namespace detail {
+inline int find_field(const std::vector<std::string>& fs, const char* name) {
+  for (size_t j = 0; j < fs.size(); ++j)
+    if (fs[j] == name) return static_cast<int>(j);
+  return -1;
+}
+template <class Bytes, class T>
+bool append(const Bytes& b, std::vector<T>& out, size_t n) {
+  if (b.size() != n * sizeof(T)) return false;
+  const size_t old = out.size();
+  out.resize(old + n);
+  if (n) std::memcpy(out.data() + old, b.data(), b.size());
+  return true;
+}
+}  // namespace detail
+
+// Decode a trainer MicroBatch into PackedBatch. Returns SF_TM_OK or
+// SF_TM_CONFIG_ERROR with *err (missing field, ragged payload sizes).
+template <class MicroBatchT>
+int pack_trainer_batch(const MicroBatchT& b, int group_size, PackedBatch& out, std::string* err) {
+  using detail::find_field;
+  const auto& fs = b.field_set;
+  const int jr = find_field(fs, "response"), jl = find_field(fs, "logp"), jf = find_field(fs, "ref_logp");
+  const int ja = find_field(fs, "advantage"), jw = find_field(fs, "reward"), jm = find_field(fs, "loss_mask");
+  const int jg = find_field(fs, "group");
+  if (jr < 0 || jl < 0 || jf < 0 || (ja < 0 && jw < 0)) {
+    if (err) *err = "trainer field set needs response, logp, ref_logp and advantage or reward";
+    return SF_TM_CONFIG_ERROR;
+  }
+  if (jg < 0 && ja < 0 && group_size <= 0) {
+    if (err) *err = "group ids: no 'group' field and no group_size";
+    return SF_TM_CONFIG_ERROR;
+  }
+  out = PackedBatch{};
+  out.B = static_cast<int64_t>(b.sample_ids.size());
+  out.has_advantage = ja >= 0;
+  out.has_mask = jm >= 0;
+  if (b.payloads.size() != b.sample_ids.size()) {
+    if (err) *err = "payloads missing (fetch with with_payload=true)";
+    return SF_TM_CONFIG_ERROR;
+  }
+  for (size_t i = 0; i < b.sample_ids.size(); ++i) {
+    const auto& row = b.payloads[i];
+    if (row.size() != fs.size()) {
+      if (err) *err = "payload row size != field_set size";
+      return SF_TM_CONFIG_ERROR;
+    }
+    const size_t L = row[jr].size() / sizeof(int32_t);
+    bool ok = row[jr].size() % sizeof(int32_t) == 0 && detail::append(row[jr], out.targets, L) &&
+              detail::append(row[jl], out.logp, L) && detail::append(row[jf], out.ref_logp, L) &&
+              detail::append(row[ja >= 0 ? ja : jw], out.per_sample, 1);
+    if (ok && jm >= 0) ok = detail::append(row[jm], out.mask, L);
+    if (ok && jg >= 0) ok = detail::append(row[jg], out.group_ids, 1);
+    if (!ok) {
+      if (err) *err = "sample " + std::to_string(b.sample_ids[i]) + ": payload sizes do not match response";
+      return SF_TM_CONFIG_ERROR;
+    }
+    if (jg < 0) out.group_ids.push_back(group_size > 0 ? static_cast<int32_t>((b.sample_ids[i] - 1) / group_size) : 0);
+    out.seq_lens.push_back(static_cast<int32_t>(L));
+    out.T += static_cast<int64_t>(L);
+  }
+  return SF_TM_OK;
+}
+
+// One Actor role's device-side loss: owns the sf_tm handle and pinned staging.
+class ActorLossSeam {
+ public:
+  explicit ActorLossSeam(int device = 0) { rc_ = sf_tm_create(device, &h_); }
+  ~ActorLossSeam() {
+    for (void* p : pin_) sf_tm_host_free(p);
+    if (h_) sf_tm_destroy(h_);
+  }
+  ActorLossSeam(const ActorLossSeam&) = delete;
+  ActorLossSeam& operator=(const ActorLossSeam&) = delete;
+
+  int status() const { return rc_; }
+  const char* last_error() const { return h_ ? sf_tm_last_error(h_) : "sf_tm_create failed"; }
+  sf_tm_t handle() const { return h_; }
+
+  // Decode `batch`, copy its bus fields through pinned staging, and run the
+  // fused DAPO/GRPO loss fwd+bwd on `d_logits` [T, V] (row stride V). Writes
+  // dlogits and the metrics (valid once `stream` is synchronised).
+  template <class MicroBatchT>
+  int step(const MicroBatchT& batch, const void* d_logits, int32_t dtype, int64_t V, void* d_dlogits,
+           const sf_tm_loss_params& params, float* h_metrics, void* stream, int group_size = 0,
+           float adv_eps = 1e-6f, int32_t std_mode = SF_TM_STD_UNBIASED) {
+    if (rc_ != SF_TM_OK) return rc_;
+    std::string err;
+    int rc = pack_trainer_batch(batch, group_size, packed_, &err);
+    if (rc != SF_TM_OK) {
+      err_ = err;
+      return rc;
+    }
+    const PackedBatch& p = packed_;
+    if ((rc = stage(0, p.targets.data(), p.targets.size() * 4)) || (rc = stage(1, p.logp.data(), p.T * 4)) ||
+        (rc = stage(2, p.ref_logp.data(), p.T * 4)) || (rc = stage(3, p.seq_lens.data(), p.B * 4)) ||
+        (rc = stage(4, p.per_sample.data(), p.B * 4)) || (rc = stage(5, p.group_ids.data(), p.B * 4)))
+      return rc;
+    if (p.has_mask && (rc = stage(6, p.mask.data(), p.T))) return rc;
+    return sf_tm_pg_step_host(h_, d_logits, dtype, p.T, V, V, static_cast<const int32_t*>(pin_[0]),
+                              static_cast<const float*>(pin_[1]), static_cast<const float*>(pin_[2]),
+                              p.has_mask ? static_cast<const uint8_t*>(pin_[6]) : nullptr,
+                              static_cast<const int32_t*>(pin_[3]), nullptr, static_cast<const float*>(pin_[4]),
+                              static_cast<const int32_t*>(pin_[5]), p.B, p.has_advantage ? -1.f : adv_eps,
+                              std_mode, &params, d_dlogits, V, h_metrics, stream);
+  }
+  const PackedBatch& packed() const { return packed_; }
+  const std::string& pack_error() const { return err_; }
+
+ private:
+  // Copy into the i-th pinned staging buffer (grown on demand; reused).
+  int stage(int i, const void* src, size_t bytes) {
+    if (bytes == 0) return SF_TM_OK;
+    if (pin_cap_[i] < bytes) {
+      if (pin_[i]) sf_tm_host_free(pin_[i]);
+      pin_[i] = nullptr;
+      const size_t cap = bytes + bytes / 4;
+      if (int rc = sf_tm_host_alloc(cap, &pin_[i])) return rc;
+      pin_cap_[i] = cap;
+    }
+    std::memcpy(pin_[i], src, bytes);
+    return SF_TM_OK;
+  }
+
+  sf_tm_t h_ = nullptr;
+  int rc_ = SF_TM_OK;
+  PackedBatch packed_;
+  std::string err_;
+  void* pin_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t pin_cap_[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+
+}  // namespace train_math
+}  // namespace staleflow

@@ -581,6 +581,17 @@ int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_
   return check_cuda(h, e, "sf_tm_synth_logits");
 }
 
+int sf_tm_host_alloc(size_t bytes, void** out) {
+  if (!out || bytes == 0) return SF_TM_CONFIG_ERROR;
+  *out = nullptr;
+  return cudaMallocHost(out, bytes) == cudaSuccess ? SF_TM_OK : SF_TM_INTERNAL;
+}
+
+int sf_tm_host_free(void* p) {
+  if (!p) return SF_TM_OK;
+  return cudaFreeHost(p) == cudaSuccess ? SF_TM_OK : SF_TM_INTERNAL;
+}
+
 int sf_tm_debug_force_generic(int on) {
   sftm::set_force_generic(on != 0);
   return SF_TM_OK;

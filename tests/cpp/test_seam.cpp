@@ -1,0 +1,158 @@
+// SPDX-License-Identifier: Apache-2.0
+// Exercises include/staleflow/train_math_seam.hpp.
+//   ./test_seam pack   CPU: MicroBatch payload codec (against the reference's own
+//                      staleflow::MicroBatch when built with -DSF_USE_REF_TYPES)
+//   ./test_seam gpu    B200: ActorLossSeam::step == sf_tm_pg_step_host on the same
+//                      packed arrays (bitwise metrics and dlogits)
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifdef SF_USE_REF_TYPES
+#include "staleflow/types.hpp"  // /root/reference/proj/include (drop-in check)
+using staleflow::Bytes;
+using staleflow::MicroBatch;
+#else
+namespace mirror {  // same member names as proj/include/staleflow/types.hpp:48-59
+using Bytes = std::vector<std::uint8_t>;
+struct MicroBatch {
+  std::uint64_t batch_id = 0;
+  std::vector<std::uint64_t> sample_ids;
+  std::vector<std::string> field_set;
+  std::vector<std::int64_t> producer_versions;
+  std::vector<std::int64_t> global_steps;
+  std::vector<std::vector<Bytes>> payloads;
+};
+}  // namespace mirror
+using mirror::Bytes;
+using mirror::MicroBatch;
+#endif
+
+#include "staleflow/train_math_seam.hpp"
+
+#ifdef SF_WITH_CUDA
+#include <cuda_runtime.h>
+#endif
+
+namespace {
+template <class T>
+Bytes enc(const std::vector<T>& v) {
+  Bytes b(v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(b.data(), v.data(), b.size());
+  return b;
+}
+int fails = 0;
+#define CHECK(c)                                                 \
+  do {                                                           \
+    if (!(c)) {                                                  \
+      std::printf("CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      ++fails;                                                   \
+    }                                                            \
+  } while (0)
+
+MicroBatch make_batch(int V, int S, int Lmax, unsigned seed, bool with_adv) {
+  MicroBatch b;
+  b.field_set = with_adv ? std::vector<std::string>{"advantage", "logp", "ref_logp", "response", "reward"}
+                         : std::vector<std::string>{"logp", "ref_logp", "response", "reward"};
+  unsigned x = seed;
+  auto rnd = [&]() { x = x * 1664525u + 1013904223u; return x >> 8; };
+  for (int i = 0; i < S; ++i) {
+    const int L = 16 + static_cast<int>(rnd() % Lmax);
+    std::vector<int32_t> resp(L);
+    std::vector<float> lp(L), rl(L);
+    for (int t = 0; t < L; ++t) {
+      resp[t] = static_cast<int32_t>(rnd() % V);
+      lp[t] = -1.f - (rnd() % 1000) * 1e-3f;
+      rl[t] = lp[t] + ((rnd() % 200) - 100) * 1e-3f;
+    }
+    const float reward = (rnd() % 2) ? 1.f : 0.f, adv = ((rnd() % 200) - 100) * 1e-2f;
+    b.sample_ids.push_back(static_cast<std::uint64_t>(i + 1));
+    b.producer_versions.push_back(3);
+    b.global_steps.push_back(7);
+    if (with_adv)
+      b.payloads.push_back({enc(std::vector<float>{adv}), enc(lp), enc(rl), enc(resp), enc(std::vector<float>{reward})});
+    else
+      b.payloads.push_back({enc(lp), enc(rl), enc(resp), enc(std::vector<float>{reward})});
+  }
+  return b;
+}
+
+void test_pack() {
+  MicroBatch b = make_batch(1000, 5, 40, 7, true);
+  staleflow::train_math::PackedBatch p;
+  std::string err;
+  CHECK(staleflow::train_math::pack_trainer_batch(b, 0, p, &err) == SF_TM_OK);
+  CHECK(p.B == 5 && p.has_advantage && !p.has_mask);
+  int64_t T = 0;
+  size_t off = 0;
+  for (size_t i = 0; i < b.payloads.size(); ++i) {
+    const Bytes& resp = b.payloads[i][3];
+    const size_t L = resp.size() / 4;
+    CHECK(p.seq_lens[i] == static_cast<int32_t>(L));
+    CHECK(std::memcmp(p.targets.data() + off, resp.data(), resp.size()) == 0);
+    CHECK(std::memcmp(p.logp.data() + off, b.payloads[i][1].data(), L * 4) == 0);
+    CHECK(std::memcmp(&p.per_sample[i], b.payloads[i][0].data(), 4) == 0);
+    off += L;
+    T += static_cast<int64_t>(L);
+  }
+  CHECK(p.T == T && p.targets.size() == static_cast<size_t>(T));
+  // rewards only: group ids from sample ids
+  MicroBatch r = make_batch(1000, 8, 20, 9, false);
+  CHECK(staleflow::train_math::pack_trainer_batch(r, 4, p, &err) == SF_TM_OK);
+  CHECK(!p.has_advantage && p.group_ids.size() == 8 && p.group_ids[3] == 0 && p.group_ids[4] == 1);
+  // ragged payload is rejected with ConfigError
+  r.payloads[2][0].pop_back();
+  CHECK(staleflow::train_math::pack_trainer_batch(r, 4, p, &err) == SF_TM_CONFIG_ERROR && !err.empty());
+  r.field_set = {"logp", "response"};
+  CHECK(staleflow::train_math::pack_trainer_batch(r, 4, p, &err) == SF_TM_CONFIG_ERROR);
+  std::printf(fails ? "PACK FAILED\n" : "PACK OK\n");
+}
+
+#ifdef SF_WITH_CUDA
+void test_gpu() {
+  const int V = 32000;
+  MicroBatch b = make_batch(V, 16, 200, 11, false);
+  staleflow::train_math::ActorLossSeam seam(0);
+  CHECK(seam.status() == SF_TM_OK);
+  staleflow::train_math::PackedBatch p;
+  std::string err;
+  staleflow::train_math::pack_trainer_batch(b, 4, p, &err);
+  void *logits = nullptr, *dl1 = nullptr, *dl2 = nullptr;
+  cudaMalloc(&logits, p.T * V * 2);
+  cudaMalloc(&dl1, p.T * V * 2);
+  cudaMalloc(&dl2, p.T * V * 2);
+  CHECK(sf_tm_synth_logits(seam.handle(), logits, SF_TM_BF16, p.T, V, V, 5, 2.f, nullptr, 0.f, 0.f, 1e-3f, nullptr) == SF_TM_OK);
+  sf_tm_loss_params prm;
+  sf_tm_default_loss_params(&prm);
+  float m1[SF_TM_NUM_METRICS], m2[SF_TM_NUM_METRICS];
+  CHECK(seam.step(b, logits, SF_TM_BF16, V, dl1, prm, m1, nullptr, 4) == SF_TM_OK);
+  cudaDeviceSynchronize();
+  // reference path: the C-ABI seam call on the same packed host arrays
+  CHECK(sf_tm_pg_step_host(seam.handle(), logits, SF_TM_BF16, p.T, V, V, p.targets.data(), p.logp.data(),
+                           p.ref_logp.data(), nullptr, p.seq_lens.data(), nullptr, p.per_sample.data(),
+                           p.group_ids.data(), p.B, 1e-6f, SF_TM_STD_UNBIASED, &prm, dl2, V, m2, nullptr) == SF_TM_OK);
+  cudaDeviceSynchronize();
+  CHECK(std::memcmp(m1, m2, sizeof(m1)) == 0);
+  CHECK(m1[SF_TM_M_ACTIVE] == static_cast<float>(p.T));
+  std::vector<unsigned char> h1(p.T * V * 2), h2(p.T * V * 2);
+  cudaMemcpy(h1.data(), dl1, h1.size(), cudaMemcpyDeviceToHost);
+  cudaMemcpy(h2.data(), dl2, h2.size(), cudaMemcpyDeviceToHost);
+  CHECK(h1 == h2);
+  cudaFree(logits);
+  cudaFree(dl1);
+  cudaFree(dl2);
+  std::printf(fails ? "GPU FAILED\n" : "GPU OK loss=%g active=%g\n", m1[0], m1[SF_TM_M_ACTIVE]);
+}
+#endif
+}  // namespace
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "pack";
+  if (mode == "pack") test_pack();
+#ifdef SF_WITH_CUDA
+  if (mode == "gpu") test_gpu();
+#endif
+  return fails ? 1 : 0;
+}

@@ -400,3 +400,18 @@ def test_full_vocab_large_batch_properties(tm, orc):
     # metrics self-consistency: recompute sum w*H from per-row outputs
     wh = float((w_tok.double() * ent.double()).sum())
     assert abs(met[3].item() - wh) <= 1e-5 * abs(wh) + 1e-6
+
+
+def test_v3_schedule_parity():
+    """The per-warp software-pipelined schedule (tm_loss3.cu, SFTM_LOSS_VARIANT=3)
+    must meet the same parity bar as the default schedule."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFTM_LOSS_VARIANT="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
+                          "test_pg_loss_fwd_bwd or test_pg_loss_deterministic or step_host"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
