@@ -35,6 +35,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tm_rowmath.cuh"
@@ -47,16 +48,25 @@ constexpr int kFW = 12;                     // forward warps (3 per SM sub-parti
 constexpr int kBW = 12;                     // backward warps (3 per SM sub-partition)
 constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
-constexpr int kCtl = kFW + kBW + 1;         // control warp: row merge, cluster exchange, scalars
-constexpr int kThreads = (kFW + kBW + 2) * 32;  // 832
+constexpr int kCtl = kFW + kBW + 1;         // control warps (2, alternating rows): merge, exchange, scalars
+constexpr int kNCtl = 2;
+constexpr int kThreads = (kFW + kBW + 1 + kNCtl) * 32;  // 864
 constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per thread = 12 KB
-constexpr int kSlots = 17;                  // smem ring slots (204 KB)
-constexpr int kRingBytes = kSlots * kCB;
+#ifndef SFTM_RING_SLOTS
+#define SFTM_RING_SLOTS 8
+#endif
+constexpr int kSlots = SFTM_RING_SLOTS;     // TMA landing ring slots (96 KB)
+constexpr int kSSlots = 18 - kSlots;        // shared-memory row-store slots (120 KB)
+constexpr int kRingBytes = (kSlots + kSSlots) * kCB;  // dynamic smem: ring + smem row store
 constexpr int kSlotCols = kCB / (128 * 4);  // TMEM columns per chunk slot (24)
 constexpr int kTSlots = 512 / kSlotCols;    // 21 TMEM chunk slots (252 KB)
+constexpr int kStore = kTSlots + kSSlots;   // row-store slots: TMEM first, then smem (31)
 constexpr int kTCols = 512;
-constexpr int kMailD = 8;                   // mailbox ring depth (rows)
-constexpr int kRD = 4;                      // depth of the per-row partial / scalar rings
+constexpr int kRD = 4;                      // depth of the per-row partial / scalar rings (flow-controlled)
+// Mailbox ring depth (rows). Not flow-controlled across the cluster: with the
+// red/scal rings bounded, a CTA's control warp is at most 2*kRD+1 rows ahead
+// of its partner's mailbox reads, so 16 can never be overrun.
+constexpr int kMailD = 16;
 
 // Per-row scalars computed once by the control warp and broadcast in smem.
 struct RowScal {
@@ -65,7 +75,7 @@ struct RowScal {
   uint32_t sgn;    // 0x80008000 when dlogits entries are -p*|c0| (bf16 fast path)
   float pad;
 };
-constexpr int kMaxChunks = 14;              // row-slice chunks that keep >= 7 TMEM slots free
+constexpr int kMaxChunks = kStore - 2;      // a whole row slice must fit the row store
 
 template <typename T>
 struct Geo {
@@ -164,7 +174,11 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
                           pack_bf16x2(g[4], g[5]), pack_bf16x2(g[6], g[7])));
 }
 
-// Debug wait instrumentation: DBG_WAIT(counter, wait-expression).
+// Debug wait instrumentation: DBG_WAIT(counter, wait-expression). Compiled in
+// only with -DSFTM_WAIT_PROFILE (scripts/wait_profile.py); otherwise free.
+#ifndef SFTM_WAIT_PROFILE
+#define DBG_WAIT(ctr, expr) expr
+#else
 #define DBG_WAIT(ctr, expr)                         \
   do {                                              \
     if (dbg) {                                      \
@@ -175,10 +189,11 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
       expr;                                         \
     }                                               \
   } while (0)
+#endif
 
 template <typename T, int C>
 __global__ void __launch_bounds__(kThreads, 1)
-    loss_tmem_kernel(const RowArgs a, int64_t slice_elems) {
+    loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
   using G = Geo<T>;
   constexpr int CE = G::CE;
   constexpr int NE = G::NE;
@@ -187,14 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t ring[];
   __shared__ __align__(8) uint64_t full_bar[kSlots];
   __shared__ __align__(8) uint64_t empty_bar[kSlots];
-  __shared__ __align__(8) uint64_t tfull_bar[kTSlots];
-  __shared__ __align__(8) uint64_t tempty_bar[kTSlots];
+  __shared__ __align__(8) uint64_t tfull_bar[kStore];
+  __shared__ __align__(8) uint64_t tempty_bar[kStore];
   __shared__ __align__(8) uint64_t mail_bar[kMailD];
   __shared__ __align__(16) float4 mail[kMailD][8];
   __shared__ __align__(16) float4 red[kRD][kFW];      // per forward warp: (m2, s, w, z_target|NaN)
-  __shared__ __align__(8) uint64_t red_bar[kRD];
+  __shared__ __align__(8) uint64_t red_bar[kRD], red_free[kRD];
   __shared__ __align__(16) RowScal scal[kRD];
-  __shared__ __align__(8) uint64_t scal_bar[kRD];
+  __shared__ __align__(8) uint64_t scal_bar[kRD], scal_free[kRD];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x;
@@ -211,20 +226,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nck = (slice_len + CE - 1) / CE;
   const int nfull = slice_len / CE;
   const uint32_t ring_base = smem_u32(ring);
+  const uint32_t stash_base = ring_base + kSlots * kCB;  // smem row-store slot i = store slot kTSlots + i
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), kFT);  // every forward thread arrives
     }
-    for (int i = 0; i < kTSlots; ++i) {
+    for (int i = 0; i < kStore; ++i) {
       mbar_init(smem_u32(&tfull_bar[i]), kFT);
       mbar_init(smem_u32(&tempty_bar[i]), kFT);  // backward threads (same count)
     }
     for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
     for (int i = 0; i < kRD; ++i) {
       mbar_init(smem_u32(&red_bar[i]), kFW);  // lane 0 of each forward warp
-      mbar_init(smem_u32(&scal_bar[i]), 1);   // the control warp lane 0
+      mbar_init(smem_u32(&red_free[i]), 1);   // lane 0 of the control warp that read it
+      mbar_init(smem_u32(&scal_bar[i]), 1);   // lane 0 of the control warp that wrote it
+      mbar_init(smem_u32(&scal_free[i]), kBW);  // lane 0 of each backward warp
     }
     fence_mbar_init();
   }
@@ -238,7 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   const T* logits = static_cast<const T*>(a.logits);
+#ifdef SFTM_WAIT_PROFILE
   unsigned long long* const dbg = a.dbg;
+#else
+  unsigned long long* const dbg = nullptr;
+#endif
   unsigned long long w_a = 0, w_b = 0;  // per-role wait cycles (debug)
   const long long t_role0 = dbg ? clock64() : 0;
 
@@ -281,7 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
     const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
     const uint32_t ring_t = ring_base + 16u * ftid;
+    const uint32_t stash_t = stash_base + 16u * ftid;
     const uint32_t tm_t = tbase + tlane + tcol;
+    // row-store read-back (repair path)
+    auto load_store = [&](uint32_t q, uint4& v0r, uint4& v1r) {
+      if (q < static_cast<uint32_t>(kTSlots)) {
+        tmem_ld8(tm_t + q * static_cast<uint32_t>(kSlotCols), v0r, v1r);
+        tmem_wait_ld(v0r, v1r);
+      } else {
+        v0r = lds128(stash_t + (q - kTSlots) * kCB);
+        v1r = lds128(stash_t + (q - kTSlots) * kCB + kCB / 2);
+      }
+    };
     uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
     // per-row inputs are loaded one row ahead so their latency never sits on the row boundary
     float wn = 0.f;
@@ -298,25 +331,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         yn = __ldg(a.targets + t + ncl);
       }
       if (wcur == 0.f) continue;
-      const int64_t yl = static_cast<int64_t>(ycur) - a.vocab_start - slice_start;
-      int ck = -1, jt = 0;
-      if (yl >= 0 && yl < slice_len) {
-        const int r = static_cast<int>(yl % CE);
-        const int v = r >= G::HALF ? 1 : 0;
-        const int rr = r - v * G::HALF;
-        if (rr / EV == ftid) {
-          ck = static_cast<int>(yl / CE);
-          jt = v * EV + rr % EV;
-        }
-      }
-      // online state with 4 independent partial sums (ILP), kept across chunks
+      (void)ycur;
       float m2 = 0.f;
       // two float2 partial sums = 4 independent chains, updated with FADD2/FFMA2
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t ts0 = ts;
-      float zyt = __int_as_float(0x7fc00000);
-      for (int k = 0; k < nck; ++k) {
+      // One chunk: smem -> registers (slot released at once) -> TMEM stash ->
+      // online softmax. `first` sets the exponent base from this thread's max of
+      // chunk 0; `partial` masks elements past the slice end. Both are constants
+      // at every call site, so the hot loop carries no per-chunk branches.
+      auto chunk = [&](int k, bool first, bool partial) {
         DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
         const uint32_t sa = ring_t + slot * kCB;
         uint4 v0 = lds128(sa);
@@ -326,29 +351,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           slot = 0;
           ph ^= 1u;
         }
-        // stash the raw words in TMEM for the backward warps
         DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
-        tc_fence_after();
-        tmem_st8(tm_t + ts * static_cast<uint32_t>(kSlotCols), v0, v1);
+        const bool in_tmem = ts < kTSlots;
+        if (in_tmem) {
+          tc_fence_after();
+          if (!(dbg_mode & 8)) tmem_st8(tm_t + ts * static_cast<uint32_t>(kSlotCols), v0, v1);
+        } else {
+          const uint32_t sa2 = stash_t + (ts - kTSlots) * kCB;
+          sts128(sa2, v0);
+          sts128(sa2 + kCB / 2, v1);
+        }
         float x[NE];
         unpack(logits, v0, v1, x);
-        if (k == 0) {
-          // base of the row's exponent arguments: this thread's max of chunk 0.
-          // Later elements may exceed it (arguments > 0 are fine); only a jump
-          // of > 126 in log2 units overflows, which the row-end repair handles.
+        const int rem = slice_len - k * CE;
+        if (first) {
+          // Later elements may exceed this base (arguments > 0 are fine); only a
+          // jump of > 126 in log2 units overflows, which the row-end repair handles.
           float xm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < NE; ++j)
-            if (elem_off<T>(ftid, j) < slice_len) xm = fmaxf(xm, x[j]);
+            if (!partial || elem_off<T>(ftid, j) < rem) xm = fmaxf(xm, x[j]);
           m2 = xm * c;
           if (!(m2 > -INFINITY)) m2 = 0.f;  // nothing finite: any finite base works
         }
-        if (k == ck) {
-#pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (j == jt) zyt = x[j] * a.inv_tau;
-        }
-        if (k < nfull) {
+        if (!partial && (dbg_mode & 1)) {
+          s2[0].x += __uint_as_float(v0.x & 0x3fffffffu);  // debug: no math (pipeline ceiling)
+        } else if (!partial) {
           const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
@@ -358,8 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
           }
         } else {
-          // last (partial) chunk of the slice: masked, -inf safe
-          const int rem = slice_len - k * CE;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
             if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
@@ -370,13 +396,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        tmem_wait_st(v0, v1);
-        tc_fence_before();
-        mbar_arrive(tfull0 + 8u * ts);
-        if (++ts == kTSlots) {
+        if (in_tmem) {
+          if (!(dbg_mode & 8)) tmem_wait_st(v0, v1);
+          tc_fence_before();
+        }
+        mbar_arrive(tfull0 + 8u * ts);  // release: orders the smem-store writes too
+        if (++ts == kStore) {
           ts = 0;
           tph ^= 1u;
         }
+      };
+      if (nck == 0) {
+        // empty slice (a cluster wider than the vocab): contributes nothing
+      } else if (nfull == 0) {
+        chunk(0, true, true);
+      } else {
+        chunk(0, true, false);
+        for (int k = 1; k < nfull; ++k) chunk(k, false, false);
+        if (nck > nfull) chunk(nfull, false, true);
       }
       Stats my{m2, (s2[0].x + s2[1].x) + (s2[0].y + s2[1].y), (w2[0].x + w2[1].x) + (w2[0].y + w2[1].y)};
       // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
@@ -388,23 +425,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t q = ts0;
         for (int k = 0; k < nck; ++k) {
           uint4 v0r, v1r;
-          tmem_ld8(tm_t + q * static_cast<uint32_t>(kSlotCols), v0r, v1r);
-          tmem_wait_ld(v0r, v1r);
+          load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
           const int rem = slice_len - k * CE;
 #pragma unroll
           for (int j = 0; j < NE; ++j)
             if (elem_off<T>(ftid, j) < rem) mx = fmaxf(mx, x[j]);
-          if (++q == kTSlots) q = 0;
+          if (++q == kStore) q = 0;
         }
         const float mb2 = (mx == -INFINITY) ? -INFINITY : mx * c;
         float sr = 0.f, wr = 0.f;
         q = ts0;
         for (int k = 0; k < nck; ++k) {
           uint4 v0r, v1r;
-          tmem_ld8(tm_t + q * static_cast<uint32_t>(kSlotCols), v0r, v1r);
-          tmem_wait_ld(v0r, v1r);
+          load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
           const int rem = slice_len - k * CE;
@@ -417,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               wr = fmaf(e, av, wr);
             }
           }
-          if (++q == kTSlots) q = 0;
+          if (++q == kStore) q = 0;
         }
         if (bad) my = Stats{mb2, sr, wr};
       }
@@ -425,23 +460,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Per-warp partial -> smem ring; no CTA barrier: the control warp
       // merges the 12 partials, so forward warps go straight to the next row.
       my = warp_merge(my);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float oz = __shfl_xor_sync(0xffffffffu, zyt, o);
-        zyt = (zyt != zyt) ? oz : zyt;
-      }
       if (lane == 0) {
-        red[nrow % kRD][fw] = make_float4(my.m2, my.s, my.w, zyt);
+#ifndef SFTM_NO_FLOWCTL  // A/B timing only: unsafe when the forward runs > kRD rows ahead
+        mbar_wait(smem_u32(&red_free[nrow % kRD]), ((nrow / kRD) & 1u) ^ 1u);
+#endif
+        red[nrow % kRD][fw] = make_float4(my.m2, my.s, my.w, 0.f);
         mbar_arrive(smem_u32(&red_bar[nrow % kRD]));
       }
       ++nrow;
     }
-  } else if (warp == kCtl) {
+  } else if (warp >= kCtl) {
     // ================================================================ control
     // Per row: merge the 12 forward partials, exchange with the cluster through
     // DSMEM mailboxes, compute the loss scalars once and publish them to the
     // backward warps. Never touches the row data, so it runs as far ahead as
-    // the forward warps allow.
+    // the forward warps allow. Two control warps take alternating active rows
+    // so the per-row latency chain (merge -> DSMEM round trip -> scalars) of
+    // one row overlaps the next.
+    const int ci = warp - kCtl;
     const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
     const bool leader = (crank == 0 && lane == 0);
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -467,29 +503,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         yn = __ldg(a.targets + tn);
       }
       if (w == 0.f) {
-        if (leader) {
+        if (leader && ci == 0) {
           if (a.out_logp) a.out_logp[t] = 0.f;
           if (a.out_entropy) a.out_entropy[t] = 0.f;
         }
         continue;
       }
+      if (static_cast<int>(nrow % kNCtl) != ci) {  // the other control warp's row
+        ++nrow;
+        continue;
+      }
       const uint32_t rs = nrow % kRD;
       const uint32_t rpar = (nrow / kRD) & 1u;
-      const int64_t yl64 = static_cast<int64_t>(ycur) - a.vocab_start - slice_start;
+      const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
+      const int64_t yl64 = yg - slice_start;
+      // z_target straight from HBM, issued before the partials wait; the release
+      // arrive of the exchange below orders this read before any dlogits write
+      // of the row (in-place dlogits stays safe)
+      float zy = __int_as_float(0x7fc00000);
+      if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
       DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), rpar));
       Stats v = stats_empty();
-      float z = __int_as_float(0x7fc00000);
       if (lane < kFW) {
         const float4 r = red[rs][lane];
         v = Stats{r.x, r.y, r.z};
-        z = r.w;
       }
       v = warp_merge(v);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float oz = __shfl_xor_sync(0xffffffffu, z, o);
-        z = (z != z) ? oz : z;
-      }
+      if (lane == 0) mbar_arrive(smem_u32(&red_free[rs]));  // the shuffles consumed every lane's read
+      const float z = 0.f;
       const uint32_t mb = nrow % kMailD;
       if (lane == 0) {
         if (C == 1) {
@@ -511,12 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         DBG_WAIT(w_b, mbar_wait_cluster_lite(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u));
       }
       Stats st = stats_empty();
-      float zy = __int_as_float(0x7fc00000);
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const float4 mv = mail[mb][q];
         st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
-        if (!(mv.w != mv.w)) zy = mv.w;
       }
       float lse2, lse, H, logp;
       row_scalars(st, zy, lse2, lse, H, logp);
@@ -540,13 +579,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
         r.yl = (yl64 >= 0 && yl64 < slice_len) ? static_cast<int>(yl64) : -1;
         r.pad = 0.f;
+#ifndef SFTM_NO_FLOWCTL
+        mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
+#endif
         scal[rs] = r;
         mbar_arrive(smem_u32(&scal_bar[rs]));
       }
     
       ++nrow;
     }
-    if (leader) finish_metrics(a, cid, ncl, acc);
+    // fixed-order combine of the two control warps' fp64 partials, then the
+    // deterministic cross-block finish
+    __shared__ double acc_sh[8];
+    if (ci == 1 && lane == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc_sh[i] = acc[i];
+    }
+    named_bar_sync(2, kNCtl * 32);
+    if (ci == 0 && leader) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += acc_sh[i];
+      finish_metrics(a, cid, ncl, acc);
+    }
   } else {
     // ================================================================ backward
     const int btid = tid;                     // same element mapping as forward warp warp+kBW
@@ -556,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float c = a.inv_tau * kLog2e;
     const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
     const uint32_t tm_t = tbase + tlane + tcol;
+    const uint32_t stash_t = stash_base + 16u * btid;
     uint32_t ts = 0, tph = 0, nrow = 0;
     float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
     for (int64_t t = cid; t < a.T; t += ncl) {
@@ -573,6 +628,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t rpar = (nrow / kRD) & 1u;
       DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
       const RowScal rsc = scal[rs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
       int ck = -1, jt = 0;
@@ -588,24 +645,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
       const uint32_t sgn = neg ? 0x80008000u : 0u;
       const float gts = neg ? -gt : gt;  // target term before the sign flip
-      for (int k = 0; k < nck; ++k) {
+      // One chunk of dlogits. MODE (row-uniform): 0 = bf16 with |c0| folded
+      // into the exponent and the sign applied to the packed words, 1 = no
+      // entropy term, 2 = entropy term. `partial` masks past the slice end.
+      auto bchunk = [&](int k, bool partial, int mode) {
         DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
         tc_fence_after();
-        uint4 w0, w1;
-        tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
-        tmem_wait_ld(w0, w1);
-        tc_fence_before();
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
+        if (ts < kTSlots) {
+          if (!(dbg_mode & 8)) {
+            tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
+            tmem_wait_ld(w0, w1);
+          }
+          tc_fence_before();
+        } else {
+          w0 = lds128(stash_t + (ts - kTSlots) * kCB);
+          w1 = lds128(stash_t + (ts - kTSlots) * kCB + kCB / 2);
+        }
         mbar_arrive(tempty0 + 8u * ts);
-        if (++ts == kTSlots) {
+        if (++ts == kStore) {
           ts = 0;
           tph ^= 1u;
         }
+        T* dst = drow + k * CE;
+        if (!partial && (dbg_mode & 2)) {  // debug: store the words back (pipeline ceiling)
+          if (!(dbg_mode & 4)) {
+            stg128_cs(dst + EV * btid, w0);
+            stg128_cs(dst + G::HALF + EV * btid, w1);
+          }
+          return;
+        }
         float x[NE], gr[NE];
         unpack(logits, w0, w1, x);
-        T* dst = drow + k * CE;
-        const bool full = k < nfull;
-        if (G::es == 2 && c1 == 0.f) {
-          // bf16: |c0| folded into the exponent, sign applied on the packed words
+        if (mode == 0) {
           const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2f, -lse2f);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
@@ -618,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < NE; ++j)
               if (j == jt) gr[j] += gts;
           }
-          if (full) {
+          if (!partial) {
             uint4 p0, p1;
             p0.x = pack_bf16x2(gr[0], gr[1]) ^ sgn;
             p0.y = pack_bf16x2(gr[2], gr[3]) ^ sgn;
@@ -630,11 +702,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
             stg128_cs(dst + EV * btid, p0);
             stg128_cs(dst + G::HALF + EV * btid, p1);
-            continue;
+            return;
           }
 #pragma unroll
           for (int j = 0; j < NE; ++j) gr[j] = neg ? -gr[j] : gr[j];
-        } else if (c1 == 0.f) {
+        } else if (mode == 1) {
           const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2, -lse2);
           const float2 mc0 = make_float2(-c0, -c0);
 #pragma unroll
@@ -661,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (j == jt) gr[j] += gt;
           }
         }
-        if (full) {
+        if (!partial) {
           store_vec(dst + EV * btid, gr);
           store_vec(dst + G::HALF + EV * btid, gr + EV);
         } else {
@@ -672,13 +744,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (off < rem) st1(dst + off, gr[j]);
           }
         }
+      };
+      const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
+      if (mode == 0) {
+        for (int k = 0; k < nfull; ++k) bchunk(k, false, 0);
+        if (nck > nfull) bchunk(nfull, true, 0);
+      } else if (mode == 1) {
+        for (int k = 0; k < nfull; ++k) bchunk(k, false, 1);
+        if (nck > nfull) bchunk(nfull, true, 1);
+      } else {
+        for (int k = 0; k < nfull; ++k) bchunk(k, false, 2);
+        if (nck > nfull) bchunk(nfull, true, 2);
       }
       ++nrow;
     }
   }
 
   if (dbg && lane == 0) {
-    const int role = (warp == kProd) ? 0 : (warp == kCtl) ? 2 : (warp >= kBW) ? 1 : 3;
+    const int role = (warp == kProd) ? 0 : (warp >= kCtl) ? 2 : (warp >= kBW) ? 1 : 3;
     atomicAdd(dbg + 3 * role + 0, static_cast<unsigned long long>(clock64() - t_role0));
     atomicAdd(dbg + 3 * role + 1, w_a);
     atomicAdd(dbg + 3 * role + 2, w_b);
@@ -747,7 +830,11 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (C > 1) ? 1 : 0;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ad, slice);
+  static const int dbg_mode = [] {
+    const char* v = getenv("SFTM_DBG_NOCOMPUTE");  // debug: 1 = no forward math, 2 = no backward math
+    return v ? atoi(v) : 0;
+  }();
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ad, slice, dbg_mode);
   if (info) {
     info->kernel = 2;
     info->cluster = C;
@@ -758,19 +845,41 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
 }
 
 template <typename T>
+int launch_with(const RowArgs& a, int C, cudaStream_t s, LaunchInfo* info) {
+  using G = Geo<T>;
+  int64_t slice = (a.V + C - 1) / C;
+  slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
+  switch (C) {
+    case 1: return launch_c<T, 1>(a, slice, s, info);
+    case 2: return launch_c<T, 2>(a, slice, s, info);
+    case 3: return launch_c<T, 3>(a, slice, s, info);
+    case 4: return launch_c<T, 4>(a, slice, s, info);
+    case 8: return launch_c<T, 8>(a, slice, s, info);
+  }
+  return -2;
+}
+
+template <typename T>
 int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   using G = Geo<T>;
-  for (int C : {1, 2, 4, 8}) {
+  auto nck_of = [&](int C) {
     int64_t slice = (a.V + C - 1) / C;
-    slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
-    const int64_t nck = (slice + G::CE - 1) / G::CE;
-    if (nck > kMaxChunks) continue;
-    switch (C) {
-      case 1: return launch_c<T, 1>(a, slice, s, info);
-      case 2: return launch_c<T, 2>(a, slice, s, info);
-      case 4: return launch_c<T, 4>(a, slice, s, info);
-      case 8: return launch_c<T, 8>(a, slice, s, info);
-    }
+    slice = (slice + G::EV - 1) / G::EV * G::EV;
+    return (slice + G::CE - 1) / G::CE;
+  };
+  static const int forced = [] {  // tuning knob: SFTM_LOSS_C=1|2|3|4|8
+    const char* v = getenv("SFTM_LOSS_C");
+    return v ? atoi(v) : 0;
+  }();
+  if (forced && nck_of(forced) <= kMaxChunks) return launch_with<T>(a, forced, s, info);
+  // Prefer the smallest cluster whose slice leaves TMEM room for two full rows
+  // (forward(r+1) then never waits for backward(r) to free slots), then any
+  // cluster whose slice fits at all.
+  for (int C : {1, 2, 3, 4}) {
+    if (2 * nck_of(C) <= kStore) return launch_with<T>(a, C, s, info);
+  }
+  for (int C : {1, 2, 4, 8}) {
+    if (nck_of(C) <= kMaxChunks) return launch_with<T>(a, C, s, info);
   }
   return -2;  // not eligible: caller falls back
 }

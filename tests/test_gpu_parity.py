@@ -231,6 +231,15 @@ def test_pg_loss_deterministic(tm, orc):
     assert np.array_equal(d1, d2)
 
 
+@pytest.mark.parametrize("dtype,V", [("bf16", 3000), ("f32", 5000)])
+def test_pg_loss_deep_runahead(tm, orc, dtype, V):
+    """Many short rows: a row slice is one chunk, so the forward warps can run
+    up to the whole row store (31 rows) ahead of the backward warps. The
+    partial/scalar rings and the cluster mailboxes must stay flow-controlled."""
+    prob = orc.synth_problem(5, [300, 257, 400, 311, 280], V, dtype, prompt_max=30)
+    check_loss_case(tm, orc, prob)
+
+
 def test_pg_loss_all_masked_and_empty(tm, orc):
     from paper_2604_11554_b200 import _lib
 
@@ -400,6 +409,23 @@ def test_full_vocab_large_batch_properties(tm, orc):
     # metrics self-consistency: recompute sum w*H from per-row outputs
     wh = float((w_tok.double() * ent.double()).sum())
     assert abs(met[3].item() - wh) <= 1e-5 * abs(wh) + 1e-6
+
+
+@pytest.mark.parametrize("C", [1, 2, 3, 4])
+def test_cluster_size_parity(C):
+    """Every cluster size the fused kernel can pick (SFTM_LOSS_C forces one)
+    meets the same parity bar, including the deep run-ahead cases."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFTM_LOSS_C=str(C))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
+                          "test_pg_loss_fwd_bwd or test_pg_loss_deterministic or deep_runahead or step_host",
+                          "--timeout", "120"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
 def test_v3_schedule_parity():
