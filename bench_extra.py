@@ -12,9 +12,11 @@ kernel, clocks):
               trainer router (a5 fwd+bwd over the config-2 micro-batch tokens)
   --config 4  Qwen3-Omni long packed sequences: 16k tokens, prompt + image/audio
               spans masked, DAPO + KL (beta 0.05), Qwen vocab bf16
-  --config 5  vocab-parallel fused loss over P = n_gpus ranks (NCCL all-gather of
-              16 B/token/rank between the two shard kernels), 4 micro-batches of
-              32 x 4096 tokens per step, staleness-tagged samples
+  --config 5  vocab-parallel fused loss over P = n_gpus ranks: one single-pass
+              kernel per rank, per-row partials exchanged in-kernel through
+              NVLink peer mailboxes (--vp-two-pass: stats kernel + NCCL
+              all_gather + backward kernel), 4 micro-batches of 32 x 4096
+              tokens per step, staleness-tagged samples
 """
 from __future__ import annotations
 
@@ -163,7 +165,8 @@ def run_loss_config(args, cfg, world, rank, dev, dist):
            "l2": "inputs >> L2 (no flush)", "parallelism": f"dp{world}"},
           {"bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
            "peak_source": src, "algorithmic_bytes_per_launch": by, "avg_launch_ms": kms,
-           "kernel": "loss_tmem_kernel"}, clocks, int(launches))
+           "kernel": "{kernel}<{t},C={cluster}> grid {grid}".format(t="bf16" if es == 2 else "f32",
+                                                                    **h.last_launch())}, clocks, int(launches))
 
 
 def run_r3(args, world, rank, dev, dist):
@@ -224,7 +227,7 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     import torch
 
     from paper_2604_11554_b200 import _lib, train_math as tm
-    from paper_2604_11554_b200.vocab_parallel import gather_stats, shard_bounds
+    from paper_2604_11554_b200.vocab_parallel import gather_stats, open_peer_exchange, shard_bounds
 
     V, P = 151936, world
     b = shard_bounds(V, P)
@@ -257,10 +260,28 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     stream = torch.cuda.current_stream(dev)
     h = tm.handle(dev.index)
 
+    fused = not args.vp_two_pass
+    if fused and P > 1:
+        open_peer_exchange()
+
     def step(rec):
         ev = []
         for m in range(M):
             sl = slice(m * T_mb, (m + 1) * T_mb)
+            if fused:
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if rec else None
+                if rec:
+                    e[0].record(stream)
+                if P > 1:
+                    tm.vp_fused_loss_fwd_bwd(shard, vs, targets[sl], old[sl], ref[sl], adv_tok[sl], w_tok[sl],
+                                             params, dlogits=dsh, metrics=metrics[m])
+                else:
+                    tm.pg_loss_fwd_bwd(shard, targets[sl], old[sl], ref[sl], adv_tok[sl], w_tok[sl], params,
+                                       dlogits=dsh, metrics=metrics[m])
+                if rec:
+                    e[1].record(stream)
+                    ev.append((e[0], e[1]))
+                continue
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if rec else None
             if rec:
                 e[0].record(stream)
@@ -284,19 +305,24 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     act_mb = n_act / M
     # algorithmic (minimum) bytes per rank per micro-batch: read the shard once, write its dlogits once
     by_min = act_mb * 4 * Vp + (T_mb - act_mb) * 2 * Vp
-    # this design's two kernels read the active shard rows twice (stats, then backward)
-    by_design = act_mb * 6 * Vp + (T_mb - act_mb) * 2 * Vp
-    per_mb_ms = kms * 2  # kms averages the two kernels
+    # two-pass: the two kernels read the active shard rows twice (stats, then backward)
+    by_design = by_min if fused else act_mb * 6 * Vp + (T_mb - act_mb) * 2 * Vp
+    per_mb_ms = kms if fused else kms * 2  # two-pass: kms averages the two kernels
     ach = by_min / (per_mb_ms / 1e3) / 1e9
     if rank == 0:
         _line(args, world, "tokens/s vocab-parallel fused logprob+GRPO loss fwd+bwd (Qwen3-4B vocab)",
               T / (ms_step / 1e3), ms_step, "bf16",
               {"workload": f"vocab-parallel P={P}: 4 x (32 x 4096 tok), shard V/P={Vp}, staleness-tagged samples",
                "config_index": 5, "tokens_per_step": T, "vocab": V, "vocab_shard": Vp,
-               "parallelism": f"vocab-parallel tp{P} (NCCL all-gather 16 B/token/rank)", "_scaling": "strong",
+               "parallelism": (f"vocab-parallel tp{P} (" + ("in-kernel peer-mailbox exchange over NVLink, 32 B/row/peer"
+                                                             if fused else "NCCL all-gather 16 B/token/rank") + ")"),
+               "_scaling": "strong",
                "staleness_hist": stale_hist},
               {"bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
                "peak_source": src, "algorithmic_bytes_per_launch_pair": by_min, "design_bytes": by_design,
-               "avg_kernel_ms": kms, "kernel": "rows_ring_kernel<bf16, VpStats|VpBwd>",
-               "bytes_model": "algorithmic 4V/P per active token (read+write once); design reads the shard twice"},
+               "avg_kernel_ms": kms,
+               "kernel": ("{kernel}<bf16,C={cluster}> grid {grid}".format(**h.last_launch()) if fused
+                          else "rows_ring_kernel<bf16, VpStats|VpBwd>"),
+               "bytes_model": "algorithmic 4V/P per active token (read+write once)" +
+                              ("" if fused else "; the two-pass design reads the shard twice")},
               clocks, int(launches))

@@ -115,6 +115,12 @@ int sf_tm_abi_version(void);
 /* Number of kernel launches issued on this handle since creation (evidence for
  * the bench's gpu_launches count). */
 uint64_t sf_tm_launch_count(sf_tm_t h);
+/* Which row kernel the last row-kernel call on this handle launched:
+ * *kernel 0 = streaming TMA ring, 1 = generic two-pass, 2 = fused TMEM/smem
+ * row-store loss kernel, 3 = its per-warp pipelined variant, 4 = the fused
+ * vocab-parallel (peer-mailbox) kernel; *cluster = CTAs
+ * per row; *grid = CTAs launched. Any pointer may be NULL. */
+int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* grid);
 
 /* ---- a6: varlen packing metadata --------------------------------------
  * seq_lens[B] (>= 0), prompt_lens[B] (optional; tokens [0, prompt_len) of a
@@ -228,6 +234,31 @@ int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, in
                           const float* ref_logp, const float* adv_tok, const float* w_tok,
                           const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
                           float* out_metrics, float* out_logp, float* out_entropy, void* stream);
+
+/* ---- a7 fused: vocab-parallel with the exchange inside the kernel --------
+ * The two-pass path above reads each shard row twice (stats, then backward:
+ * 6V/P bytes per token per rank) with an NCCL all_gather in between. The
+ * fused path reads it once (4V/P): every rank runs one persistent kernel on
+ * its shard with the same row schedule, and the per-row partial statistics
+ * travel between the ranks' control warps through peer-mapped mailboxes
+ * (NVLink P2P stores with system-scope release/acquire).
+ *
+ * Setup, once per process group (any transport for the 64-byte handles):
+ *   sf_tm_vp_mailbox_create(h, P, rank, my_handle);        // allocates + exports
+ *   all-gather the P handles in rank order (P * SF_TM_IPC_HANDLE_BYTES bytes);
+ *   sf_tm_vp_mailbox_open(h, all_handles);                 // maps the peers
+ * Then every rank calls sf_tm_vp_fused_loss_fwd_bwd with the same T, w_tok and
+ * call sequence (calls are matched by order). Outputs are as
+ * sf_tm_vp_loss_fwd_bwd; metrics, logp and entropy are identical on all ranks.
+ * A rank whose peers never launch traps after 20 s (no silent hang). */
+#define SF_TM_IPC_HANDLE_BYTES 64
+int sf_tm_vp_mailbox_create(sf_tm_t h, int32_t P, int32_t rank, void* ipc_handle_out);
+int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles);
+int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp,
+                                int64_t ld, int64_t vocab_start, const int32_t* targets, const float* old_logp,
+                                const float* ref_logp, const float* adv_tok, const float* w_tok,
+                                const sf_tm_loss_params* params, void* dlogits, int64_t ld_d, float* out_metrics,
+                                float* out_logp, float* out_entropy, void* stream);
 
 /* ---- pinned host staging (for the C++ seam adapter) ----------------------
  * Page-locked host memory so the seam's H2D copies are asynchronous DMA.

@@ -55,6 +55,8 @@ class LossParams(ctypes.Structure):
     ]
 
 
+IPC_HANDLE_BYTES = 64  # SF_TM_IPC_HANDLE_BYTES
+
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
@@ -69,6 +71,7 @@ _SIGS = {
     "sf_tm_destroy": (ctypes.c_int, [_H]),
     "sf_tm_last_error": (ctypes.c_char_p, [_H]),
     "sf_tm_launch_count": (_u64, [_H]),
+    "sf_tm_last_launch": (_i32, [_H, _vp, _vp, _vp]),
     "sf_tm_varlen_meta": (ctypes.c_int, [_H, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sf_tm_grpo_advantage": (ctypes.c_int, [_H, _vp, _vp, _i64, _f32, _i32, _vp, _vp, _vp]),
     "sf_tm_logprob_fwd": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _vp]),
@@ -88,6 +91,13 @@ _SIGS = {
     "sf_tm_vp_loss_fwd_bwd": (
         ctypes.c_int,
         [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
+         ctypes.POINTER(LossParams), _vp, _i64, _vp, _vp, _vp, _vp],
+    ),
+    "sf_tm_vp_mailbox_create": (ctypes.c_int, [_H, _i32, _i32, _vp]),
+    "sf_tm_vp_mailbox_open": (ctypes.c_int, [_H, _vp]),
+    "sf_tm_vp_fused_loss_fwd_bwd": (
+        ctypes.c_int,
+        [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
          ctypes.POINTER(LossParams), _vp, _i64, _vp, _vp, _vp, _vp],
     ),
     "sf_tm_synth_logits": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _u64, _f32, _vp, _f32, _f32, _f32, _vp]),

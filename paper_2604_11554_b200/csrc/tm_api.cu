@@ -20,6 +20,14 @@ struct sf_tm_handle {
   int device = 0;
   std::string err;
   uint64_t launches = 0;
+  sftm::LaunchInfo last;  // last row-kernel launch (sf_tm_last_launch)
+  // fused vocab-parallel peer mailboxes (sf_tm_vp_mailbox_*)
+  void* xp_local = nullptr;
+  void* xp_mail[sftm::kXpMaxP] = {};
+  int xp_P = 0, xp_rank = -1;
+  bool xp_ready = false;
+  unsigned long long xp_epoch = 0;
+  int* xp_err = nullptr;
   // metric partials for the deterministic row-kernel reduction
   double* partials = nullptr;
   unsigned* ticket = nullptr;
@@ -148,6 +156,7 @@ int run_rows(sf_tm_t h, sftm::RowArgs& a, int mode, cudaStream_t s, const char* 
   sftm::LaunchInfo info;
   const int e = sftm::launch_rows(a, mode, s, &h->err, &info);
   h->launches += static_cast<uint64_t>(info.launches);
+  if (info.launches) h->last = info;
   return check_cuda(h, e, where);
 }
 
@@ -214,6 +223,10 @@ int sf_tm_destroy(sf_tm_t h) {
                   h->d_rewards, h->d_gids, h->d_cu,    h->d_adv,  h->d_total,   h->d_metrics};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int q = 0; q < h->xp_P; ++q)
+    if (q != h->xp_rank && h->xp_mail[q]) cudaIpcCloseMemHandle(h->xp_mail[q]);
+  if (h->xp_local) cudaFree(h->xp_local);
+  if (h->xp_err) cudaFree(h->xp_err);
   delete h;
   return SF_TM_OK;
 }
@@ -221,6 +234,14 @@ int sf_tm_destroy(sf_tm_t h) {
 const char* sf_tm_last_error(sf_tm_t h) { return h ? h->err.c_str() : "null handle"; }
 
 uint64_t sf_tm_launch_count(sf_tm_t h) { return h ? h->launches : 0; }
+
+int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* grid) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (kernel) *kernel = h->last.kernel;
+  if (cluster) *cluster = h->last.cluster;
+  if (grid) *grid = h->last.grid;
+  return SF_TM_OK;
+}
 
 int sf_tm_varlen_meta(sf_tm_t h, const int32_t* seq_lens, const int32_t* prompt_lens,
                       const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,
@@ -560,6 +581,108 @@ int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, in
   a.out_logp = out_logp;
   a.out_entropy = out_entropy;
   return run_rows(h, a, sftm::kModeVpBwd, s, "sf_tm_vp_loss_fwd_bwd");
+}
+
+int sf_tm_vp_mailbox_create(sf_tm_t h, int32_t P, int32_t rank, void* ipc_handle_out) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (P < 1 || P > sftm::kXpMaxP) return fail(h, SF_TM_CONFIG_ERROR, "P must be in [1, 8]");
+  if (rank < 0 || rank >= P) return fail(h, SF_TM_CONFIG_ERROR, "rank must be in [0, P)");
+  if (!ipc_handle_out) return fail(h, SF_TM_CONFIG_ERROR, "ipc_handle_out is required");
+  if (h->xp_local) return fail(h, SF_TM_CONFIG_ERROR, "mailbox already created on this handle");
+  cudaError_t e = cudaMalloc(&h->xp_local, sftm::kXpMailboxBytes);
+  if (e == cudaSuccess) e = cudaMemset(h->xp_local, 0, sftm::kXpMailboxBytes);
+  if (e == cudaSuccess) e = cudaMalloc(&h->xp_err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(h->xp_err, 0, sizeof(int));
+  cudaIpcMemHandle_t ih;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&ih, h->xp_local);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return check_cuda(h, e, "sf_tm_vp_mailbox_create");
+  std::memcpy(ipc_handle_out, &ih, SF_TM_IPC_HANDLE_BYTES);
+  h->xp_P = P;
+  h->xp_rank = rank;
+  h->xp_mail[rank] = h->xp_local;
+  return SF_TM_OK;
+}
+
+int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (!h->xp_local) return fail(h, SF_TM_CONFIG_ERROR, "sf_tm_vp_mailbox_create first");
+  if (h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "mailboxes already open");
+  if (!ipc_handles) return fail(h, SF_TM_CONFIG_ERROR, "ipc_handles is required");
+  const uint8_t* hb = static_cast<const uint8_t*>(ipc_handles);
+  for (int q = 0; q < h->xp_P; ++q) {
+    if (q == h->xp_rank) continue;
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, hb + static_cast<size_t>(q) * SF_TM_IPC_HANDLE_BYTES, SF_TM_IPC_HANDLE_BYTES);
+    const cudaError_t e = cudaIpcOpenMemHandle(&h->xp_mail[q], ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      h->xp_mail[q] = nullptr;
+      return check_cuda(h, e, "sf_tm_vp_mailbox_open (cudaIpcOpenMemHandle)");
+    }
+  }
+  h->xp_ready = true;
+  return SF_TM_OK;
+}
+
+int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp,
+                                int64_t ld, int64_t vocab_start, const int32_t* targets, const float* old_logp,
+                                const float* ref_logp, const float* adv_tok, const float* w_tok,
+                                const sf_tm_loss_params* params, void* dlogits, int64_t ld_d, float* out_metrics,
+                                float* out_logp, float* out_entropy, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (!h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "peer mailboxes not open (sf_tm_vp_mailbox_open)");
+  if (int rc = check_rows(h, logits_shard, dtype, T, Vp, ld, targets)) return rc;
+  if (int rc = check_loss_params(h, params)) return rc;
+  if (vocab_start < 0) return fail(h, SF_TM_CONFIG_ERROR, "vocab_start must be >= 0");
+  if (!out_metrics) return fail(h, SF_TM_CONFIG_ERROR, "out_metrics is required");
+  if (ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= Vp");
+  const int64_t es = dtype == SF_TM_BF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(logits_shard) | reinterpret_cast<uintptr_t>(dlogits)) % 16 ||
+      (ld * es) % 16 || (ld_d * es) % 16)
+    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows and strides");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ++h->xp_epoch;  // every rank calls in the same order, so epochs agree
+  if (T == 0) {
+    return check_cuda(h, cudaMemsetAsync(out_metrics, 0, sizeof(float) * SF_TM_NUM_METRICS, s),
+                      "sf_tm_vp_fused_loss_fwd_bwd");
+  }
+  if (!old_logp || !ref_logp || !adv_tok || !w_tok || !dlogits)
+    return fail(h, SF_TM_CONFIG_ERROR, "missing required pointer");
+  sftm::RowArgs a;
+  a.logits = logits_shard;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = Vp;
+  a.ld = ld;
+  a.vocab_start = vocab_start;
+  a.targets = targets;
+  a.old_logp = old_logp;
+  a.ref_logp = ref_logp;
+  a.adv_tok = adv_tok;
+  a.w_tok = w_tok;
+  fill_loss(a, params);
+  a.dlogits = dlogits;
+  a.ld_d = ld_d;
+  a.out_metrics = out_metrics;
+  a.out_logp = out_logp;
+  a.out_entropy = out_entropy;
+  for (int q = 0; q < h->xp_P; ++q) a.xp_mail[q] = h->xp_mail[q];
+  a.xp_P = h->xp_P;
+  a.xp_rank = h->xp_rank;
+  a.xp_epoch = h->xp_epoch;
+  a.xp_err = h->xp_err;
+  a.partials = h->partials;
+  a.ticket = h->ticket;
+  a.max_partial_blocks = h->max_partial_blocks;
+  sftm::LaunchInfo info;
+  const int e = sftm::launch_loss_xp(a, s, &info);
+  if (e == -2) return fail(h, SF_TM_CONFIG_ERROR, "shard row too wide for the fused vocab-parallel kernel");
+  h->launches += static_cast<uint64_t>(info.launches);
+  if (info.launches) h->last = info;
+  return check_cuda(h, e, "sf_tm_vp_fused_loss_fwd_bwd");
 }
 
 int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,

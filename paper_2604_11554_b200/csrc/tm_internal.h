@@ -41,6 +41,12 @@ struct RowArgs {
   const float* gathered = nullptr;  // VpBwd: [P,T,4]
   int P = 1;
   float* out_metrics = nullptr;
+  // fused vocab-parallel exchange (sf_tm_vp_fused_loss_fwd_bwd): every rank's
+  // peer-mapped mailbox buffer, indexed by rank (xp_mail[xp_rank] is local)
+  void* xp_mail[8] = {};
+  int xp_rank = 0, xp_P = 0;
+  unsigned long long xp_epoch = 0;  // launch sequence number, identical on all ranks
+  int* xp_err = nullptr;            // set to 1 before trapping on an exchange timeout
   // optional wait-time instrumentation (debug only): per-role clock64 sums
   unsigned long long* dbg = nullptr;
   // workspace (owned by the handle)
@@ -48,6 +54,24 @@ struct RowArgs {
   unsigned* ticket = nullptr;
   int max_partial_blocks = 0;
 };
+
+// Peer mailbox geometry (fused vocab-parallel). One message = 32 B:
+// {m2, s, w, z_target|NaN} + a 64-bit tag (epoch << 32 | row + 1), written with
+// a system-scope release so a peer's acquire of the tag sees the data.
+constexpr int kXpMaxP = 8;
+constexpr int kXpMaxCtas = 256;
+constexpr int kXpMailD = 16;
+struct alignas(32) XpMsg {
+  float v[4];
+  unsigned long long tag;
+  unsigned long long pad;
+};
+// halves alternate by epoch parity so a rank one launch ahead never overwrites
+// messages a slower peer has not read yet
+constexpr size_t kXpMailboxBytes = size_t(2) * kXpMaxCtas * kXpMailD * kXpMaxP * sizeof(XpMsg);
+__host__ __device__ inline size_t xp_index(unsigned long long epoch, int cta, int slot, int src) {
+  return ((static_cast<size_t>(epoch & 1) * kXpMaxCtas + cta) * kXpMailD + slot) * kXpMaxP + src;
+}
 
 struct LaunchInfo {
   int kernel = 0;  // 0 = ring (TMA) kernel, 1 = generic two-pass kernel
@@ -59,6 +83,9 @@ struct LaunchInfo {
 // Launches the row kernel for `mode`. Returns 0 or a cudaError_t value; on a
 // config problem returns -1 with *err set.
 int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, LaunchInfo* info);
+// Fused vocab-parallel loss (one CTA per SM, peer-mailbox exchange); -2 if the
+// shard is not eligible (then the caller reports a config error).
+int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info);
 
 // Forces the generic (non-TMA) kernel; used by tests to cover both paths.
 void set_force_generic(bool on);

@@ -49,7 +49,10 @@ constexpr int kBW = 12;                     // backward warps (3 per SM sub-part
 constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
 constexpr int kCtl = kFW + kBW + 1;         // control warps (2, alternating rows): merge, exchange, scalars
-constexpr int kNCtl = 2;
+#ifndef SFTM_NCTL
+#define SFTM_NCTL 2
+#endif
+constexpr int kNCtl = SFTM_NCTL;
 constexpr int kThreads = (kFW + kBW + 1 + kNCtl) * 32;  // 864
 constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per thread = 12 KB
 #ifndef SFTM_RING_SLOTS
@@ -67,6 +70,7 @@ constexpr int kRD = 4;                      // depth of the per-row partial / sc
 // red/scal rings bounded, a CTA's control warp is at most 2*kRD+1 rows ahead
 // of its partner's mailbox reads, so 16 can never be overrun.
 constexpr int kMailD = 16;
+static_assert(kMailD == kXpMailD, "peer mailbox ring depth must match the cluster mailbox ring");
 
 // Per-row scalars computed once by the control warp and broadcast in smem.
 struct RowScal {
@@ -191,9 +195,15 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
   } while (0)
 #endif
 
-template <typename T, int C>
+// XP (C == 1 only): vocab-parallel across GPUs. Each rank runs this kernel on
+// its vocab shard with the same grid and row schedule; CTA i of every rank
+// handles the same rows, and the control warps exchange the per-row partial
+// statistics through peer-mapped global-memory mailboxes (NVLink P2P stores,
+// system-scope release/acquire) instead of DSMEM. The shard is read once.
+template <typename T, int C, bool XP = false>
 __global__ void __launch_bounds__(kThreads, 1)
     loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
+  static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
   using G = Geo<T>;
   constexpr int CE = G::CE;
   constexpr int NE = G::NE;
@@ -346,11 +356,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sa = ring_t + slot * kCB;
         uint4 v0 = lds128(sa);
         uint4 v1 = lds128(sa + kCB / 2);
-        mbar_arrive(empty0 + 8u * slot);  // release semantics order the reads first
-        if (++slot == kSlots) {
-          slot = 0;
-          ph ^= 1u;
-        }
         DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
         const bool in_tmem = ts < kTSlots;
         if (in_tmem) {
@@ -360,6 +365,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa2 = stash_t + (ts - kTSlots) * kCB;
           sts128(sa2, v0);
           sts128(sa2 + kCB / 2, v1);
+        }
+        // Release the ring slot only now: the row-store write above consumed
+        // v0/v1, so both LDS have returned. An arrive issued straight after the
+        // LDS can overtake them (SASS issues SYNCS.ARRIVE without a scoreboard
+        // wait) and the next TMA fill of the slot then races the reads.
+        mbar_arrive(empty0 + 8u * slot);
+        if (++slot == kSlots) {
+          slot = 0;
+          ph ^= 1u;
         }
         float x[NE];
         unpack(logits, v0, v1, x);
@@ -532,6 +546,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&red_free[rs]));  // the shuffles consumed every lane's read
       const float z = 0.f;
       const uint32_t mb = nrow % kMailD;
+      Stats st = stats_empty();
+      if constexpr (XP) {
+        // lane q posts this rank's partial into rank q's mailbox (q == own rank:
+        // local), then polls the message from rank q in its own mailbox
+        const unsigned long long tag = (a.xp_epoch << 32) | static_cast<unsigned long long>(nrow + 1);
+        float4 mv = make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fc00000));
+        if (lane < a.xp_P) {
+          XpMsg* dst = static_cast<XpMsg*>(a.xp_mail[lane]) + xp_index(a.xp_epoch, static_cast<int>(cid), mb, a.xp_rank);
+          st_sys_v4(dst->v, v.m2, v.s, v.w, zy);
+          st_release_sys_u64(&dst->tag, tag);
+          const XpMsg* src = static_cast<const XpMsg*>(a.xp_mail[a.xp_rank]) +
+                             xp_index(a.xp_epoch, static_cast<int>(cid), mb, lane);
+          if (ld_acquire_sys_u64(&src->tag) != tag) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_sys_u64(&src->tag) != tag) {
+              __nanosleep(200);
+              if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a peer never launched
+                if (a.xp_err) atomicExch(a.xp_err, 1);
+                __trap();
+              }
+            }
+          }
+          mv = ld_sys_v4(src->v);
+        }
+        // merge in rank order (identical scalars on every rank); the owner's z_target
+        for (int q = 0; q < a.xp_P; ++q) {
+          const float m2q = __shfl_sync(0xffffffffu, mv.x, q);
+          const float sq = __shfl_sync(0xffffffffu, mv.y, q);
+          const float wq = __shfl_sync(0xffffffffu, mv.z, q);
+          const float zq = __shfl_sync(0xffffffffu, mv.w, q);
+          st = stats_merge(st, Stats{m2q, sq, wq});
+          if (zq == zq) zy = zq;
+        }
+      } else {
       if (lane == 0) {
         if (C == 1) {
           mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
@@ -551,12 +599,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         DBG_WAIT(w_b, mbar_wait_cluster_lite(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u));
       }
-      Stats st = stats_empty();
 #pragma unroll
       for (int q = 0; q < C; ++q) {
         const float4 mv = mail[mb][q];
         st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
       }
+      }  // !XP
       float lse2, lse, H, logp;
       row_scalars(st, zy, lse2, lse, H, logp);
       float g, gH, m[8];
@@ -628,8 +676,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t rpar = (nrow / kRD) & 1u;
       DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
       const RowScal rsc = scal[rs];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
       int ck = -1, jt = 0;
@@ -652,17 +698,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
         tc_fence_after();
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
-        if (ts < kTSlots) {
+        // TMEM slots are released once tcgen05.wait::ld returned; smem-store
+        // slots only after the dlogits stores below consumed the LDS results
+        // (see the forward's ring release)
+        const uint32_t rel = tempty0 + 8u * ts;
+        const bool late = ts >= kTSlots;
+        if (!late) {
           if (!(dbg_mode & 8)) {
             tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
             tmem_wait_ld(w0, w1);
           }
           tc_fence_before();
+          mbar_arrive(rel);
         } else {
           w0 = lds128(stash_t + (ts - kTSlots) * kCB);
           w1 = lds128(stash_t + (ts - kTSlots) * kCB + kCB / 2);
         }
-        mbar_arrive(tempty0 + 8u * ts);
         if (++ts == kStore) {
           ts = 0;
           tph ^= 1u;
@@ -672,6 +723,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!(dbg_mode & 4)) {
             stg128_cs(dst + EV * btid, w0);
             stg128_cs(dst + G::HALF + EV * btid, w1);
+          }
+          if (late) {
+            __threadfence_block();  // debug path: order the LDS before the release
+            mbar_arrive(rel);
           }
           return;
         }
@@ -702,6 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
             stg128_cs(dst + EV * btid, p0);
             stg128_cs(dst + G::HALF + EV * btid, p1);
+            if (late) mbar_arrive(rel);
             return;
           }
 #pragma unroll
@@ -743,7 +799,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int off = elem_off<T>(btid, j);
             if (off < rem) st1(dst + off, gr[j]);
           }
+          __threadfence_block();  // the masked tail may store nothing: order the LDS before the release
         }
+        if (late) mbar_arrive(rel);
       };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
       if (mode == 0) {
@@ -756,6 +814,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < nfull; ++k) bchunk(k, false, 2);
         if (nck > nfull) bchunk(nfull, true, 2);
       }
+      // the row's stores consumed every lane's scalars (the fence covers rows
+      // with nothing to store): free the scal slot
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;
     }
   }
@@ -777,9 +840,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
-template <typename T, int C>
+template <typename T, int C, bool XP = false>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  auto kern = loss_tmem_kernel<T, C>;
+  auto kern = loss_tmem_kernel<T, C, XP>;
   static int max_active = -1;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -814,6 +877,7 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
     }
   }
   int64_t ncl = a.T < max_active ? a.T : max_active;
+  if (XP) ncl = max_active < kXpMaxCtas ? max_active : kXpMaxCtas;  // same grid on every rank, whatever T
   RowArgs ad = a;
   ad.dbg = debug_counters();
   if (ncl > a.max_partial_blocks) ncl = a.max_partial_blocks;
@@ -836,7 +900,7 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   }();
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ad, slice, dbg_mode);
   if (info) {
-    info->kernel = 2;
+    info->kernel = XP ? 4 : 2;
     info->cluster = C;
     info->grid = static_cast<int>(ncl * C);
     info->launches = 1;
@@ -872,13 +936,10 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
     return v ? atoi(v) : 0;
   }();
   if (forced && nck_of(forced) <= kMaxChunks) return launch_with<T>(a, forced, s, info);
-  // Prefer the smallest cluster whose slice leaves TMEM room for two full rows
-  // (forward(r+1) then never waits for backward(r) to free slots), then any
-  // cluster whose slice fits at all.
-  for (int C : {1, 2, 3, 4}) {
-    if (2 * nck_of(C) <= kStore) return launch_with<T>(a, C, s, info);
-  }
-  for (int C : {1, 2, 4, 8}) {
+  // Smallest cluster whose slice fits the row store: measured on B200, the
+  // cluster exchange costs more than the extra run-ahead a narrower slice buys
+  // (Qwen3 bf16: C=1 88% vs C=2 84% of HBM copy bandwidth, same box).
+  for (int C : {1, 2, 3, 4, 8}) {
     if (nck_of(C) <= kMaxChunks) return launch_with<T>(a, C, s, info);
   }
   return -2;  // not eligible: caller falls back
@@ -889,6 +950,19 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
 int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   if (a.dtype == 1) return loss::launch_t<uint16_t>(a, s, info);
   return loss::launch_t<float>(a, s, info);
+}
+
+int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
+  // one CTA per row per rank: the whole shard row slice must fit the row store
+  auto go = [&](auto tag) -> int {
+    using T = decltype(tag);
+    using G = loss::Geo<T>;
+    int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
+    if ((slice + G::CE - 1) / G::CE > loss::kMaxChunks) return -2;
+    return loss::launch_c<T, 1, true>(a, slice, s, info);
+  };
+  if (a.dtype == 1) return go(uint16_t{});
+  return go(float{});
 }
 
 }  // namespace sftm

@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
     const float c = a.inv_tau * kLog2e;
     uint32_t slot = 0, ph = 0;  // smem ring position (forward consumption order)
+    uint32_t rel_slot = 0;      // ring slot whose release waits for the TMEM store
     uint32_t n = 0;             // active-row counter of the forward row
     int64_t F = next_active(a.w_tok, cid, ncl, a.T, lane);  // forward row of this step
     int64_t B = -1;                                         // backward row of this step
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = ring_t + slot * kCB;
           v0 = lds128(sa);
           v1 = lds128(sa + kCB / 2);
-          mbar_arrive(empty0 + 8u * slot);
+          rel_slot = slot;  // released after tcgen05.st consumed v0/v1 (LDS returned)
           if (++slot == kSlots) {
             slot = 0;
             ph ^= 1u;
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (doF) {
           const uint32_t tsf = (n * static_cast<uint32_t>(nck) + k) % kTSlots;
           tmem_st8(tm_t + tsf * kSlotCols, v0, v1);
+          mbar_arrive(empty0 + 8u * rel_slot);
           float x[NE];
           unpack(logits, v0, v1, x);
           if (k == 0) {

@@ -56,6 +56,15 @@ class Handle:
     def launch_count(self) -> int:
         return int(_lib.lib().sf_tm_launch_count(self._h))
 
+    def last_launch(self) -> dict:
+        """The last row-kernel launch: kernel name, CTAs per row, grid."""
+        k, c, g = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        self.check(_lib.lib().sf_tm_last_launch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(g)),
+                   "sf_tm_last_launch")
+        names = {0: "rows_ring_kernel", 1: "rows_generic_kernel", 2: "loss_tmem_kernel", 3: "loss_v3_kernel",
+                 4: "loss_tmem_kernel[peer-exchange]"}
+        return {"kernel": names.get(k.value, str(k.value)), "cluster": c.value, "grid": g.value}
+
     def close(self):
         if self._h:
             _lib.lib().sf_tm_destroy(self._h)
@@ -275,6 +284,44 @@ def vp_loss_fwd_bwd(shard, vocab_start: int, gathered_stats, targets, old_logp, 
                                           ctypes.byref(params), _p(dlogits), dlogits.stride(0), _p(metrics),
                                           _p(logp), _p(ent), _stream(d))
     h.check(rc, "sf_tm_vp_loss_fwd_bwd")
+    return metrics, dlogits, logp, ent
+
+
+def vp_mailbox_create(P: int, rank: int, device: Optional[int] = None) -> bytes:
+    """Allocate this rank's peer mailbox; returns its 64-byte CUDA IPC handle."""
+    h = handle(device)
+    buf = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+    h.check(_lib.lib().sf_tm_vp_mailbox_create(h.ptr, P, rank, buf), "sf_tm_vp_mailbox_create")
+    return buf.raw
+
+
+def vp_mailbox_open(handles: list, device: Optional[int] = None):
+    """Map the peers' mailboxes (handles: every rank's 64-byte handle, rank order)."""
+    h = handle(device)
+    blob = b"".join(handles)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    h.check(_lib.lib().sf_tm_vp_mailbox_open(h.ptr, buf), "sf_tm_vp_mailbox_open")
+
+
+def vp_fused_loss_fwd_bwd(shard, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
+                          params: Optional[LossParams] = None, dlogits=None, want_logp: bool = False, metrics=None):
+    """Single-pass vocab-parallel loss: the exchange happens inside the kernel."""
+    d = _dev(shard)
+    h = handle(d)
+    dt, T, Vp, ld = _rows(shard)
+    if params is None:
+        params = default_loss_params()
+    if dlogits is None:
+        dlogits = torch.empty_like(shard)
+    if metrics is None:
+        metrics = torch.empty(_lib.NUM_METRICS, dtype=torch.float32, device=shard.device)
+    logp = torch.empty(T, dtype=torch.float32, device=shard.device) if want_logp else None
+    ent = torch.empty(T, dtype=torch.float32, device=shard.device) if want_logp else None
+    rc = _lib.lib().sf_tm_vp_fused_loss_fwd_bwd(h.ptr, _p(shard), dt, T, Vp, ld, vocab_start, _p(targets),
+                                                _p(old_logp), _p(ref_logp), _p(adv_tok), _p(w_tok),
+                                                ctypes.byref(params), _p(dlogits), dlogits.stride(0), _p(metrics),
+                                                _p(logp), _p(ent), _stream(d))
+    h.check(rc, "sf_tm_vp_fused_loss_fwd_bwd")
     return metrics, dlogits, logp, ent
 
 

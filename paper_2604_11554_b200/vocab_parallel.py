@@ -12,6 +12,12 @@ vocab-parallel LM head). One step is:
      (identical lse/entropy/logp/loss on every rank) and writes its shard's
      dlogits.
 
+`vp_fused_pg_loss_fwd_bwd` is the single-pass form (compute
+fused with its collective): one persistent kernel per rank, the per-row
+partials exchanged between the ranks' control warps through peer-mapped
+mailboxes over NVLink, so each shard row is read once (4V/P B/token/rank
+instead of 6V/P). `open_peer_exchange(group)` sets it up once per group.
+
 The exchange is a single collective (all_gather) instead of the MAX then SUM
 all-reduce pair; it carries the same information and lets every rank merge in
 the same fixed order, so the per-token scalars are bitwise identical across
@@ -62,3 +68,31 @@ def vp_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp,
     gathered = gather_stats(stats, group)
     return tm.vp_loss_fwd_bwd(shard, vocab_start, gathered, targets, old_logp, ref_logp, adv_tok, w_tok, params,
                               dlogits=dlogits, want_logp=want_logp)
+
+
+_peer_groups: dict = {}
+
+
+def open_peer_exchange(group=None) -> None:
+    """Create this rank's peer mailbox, all-gather the 64-byte CUDA IPC handles
+    over `group` (any backend) and map the peers. Idempotent per device."""
+    dev = torch.cuda.current_device()
+    if dev in _peer_groups:
+        return
+    P = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = tm.vp_mailbox_create(P, rank, dev)
+    handles = [None] * P
+    dist.all_gather_object(handles, mine, group=group)
+    tm.vp_mailbox_open(handles, dev)
+    _peer_groups[dev] = (P, rank)
+
+
+def vp_fused_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
+                             params: Optional[LossParams] = None, dlogits=None, group=None, want_logp: bool = False,
+                             metrics=None):
+    """Single-pass vocab-parallel fused loss (exchange inside the kernel over
+    NVLink peer memory); same outputs as vp_pg_loss_fwd_bwd."""
+    open_peer_exchange(group)
+    return tm.vp_fused_loss_fwd_bwd(shard, vocab_start, targets, old_logp, ref_logp, adv_tok, w_tok, params,
+                                    dlogits=dlogits, want_logp=want_logp, metrics=metrics)

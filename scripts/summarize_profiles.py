@@ -61,7 +61,8 @@ def full(tag):
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
             "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
             "smsp__warps_active.avg.per_cycle_active"]
-    md = [f"# {tag}: `ncu --set full` of the fused loss kernel (`loss_tmem_kernel<bf16, C=2>`)", "",
+    kname = raw.get("Kernel Name", ("", "loss_tmem_kernel"))[1]
+    md = [f"# {tag}: `ncu --set full` of the fused loss kernel (`{kname}`)", "",
           "Command: `python bench.py --seqs-per-mb 4 --micro-batches 1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline`",
           "(16,384 rows x V=151,936 bf16; one launch captured after warm-up). Report: "
           f"`profiles/{tag}_fused_full.ncu-rep`.", "", "| metric | value |", "|---|---|"]
@@ -81,11 +82,11 @@ def traffic(tag):
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
     vals = {r["Metric Name"]: float(r["Metric Value"].replace(",", "")) for r in rows}
     rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
-    j = {"kernel": "loss_tmem_kernel<bf16,C=2>", "vocab": 151936, "rows": 131072,
+    j = {"kernel": rows[0]["Kernel Name"], "vocab": 151936, "rows": 131072,
          "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
          "ncu_duration_ns": vals.get("gpu__time_duration.sum"),
          "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                    "-k regex:loss_tmem_kernelItLi2E -s 2 -c 1 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline",
+                    "-k regex:loss_tmem_kernelItLi1E -s 2 -c 1 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline",
          "round": tag}
     json.dump(j, open(os.path.join(PROF, "fused_loss_traffic.json"), "w"), indent=1)
     return j
