@@ -55,16 +55,17 @@ struct RowArgs {
   int max_partial_blocks = 0;
 };
 
-// Peer mailbox geometry (fused vocab-parallel). One message = 32 B:
-// {m2, s, w, z_target|NaN} + a 64-bit tag (epoch << 32 | row + 1), written with
-// a system-scope release so a peer's acquire of the tag sees the data.
+// Peer mailbox geometry (fused vocab-parallel). One message = 4 x 64-bit words
+// {m2, s, w, z_target|NaN}, each word = (32-bit tag << 32) | float bits, tag =
+// epoch << 20 | row + 1. Every word is written and read with single-copy-atomic
+// 8-byte accesses, so a reader that sees all four tags match has the whole
+// message: no fences on either side (a system-scope release per row cost more
+// than the row's HBM time at narrow shards).
 constexpr int kXpMaxP = 8;
 constexpr int kXpMaxCtas = 256;
 constexpr int kXpMailD = 16;
 struct alignas(32) XpMsg {
-  float v[4];
-  unsigned long long tag;
-  unsigned long long pad;
+  unsigned long long w[4];
 };
 // halves alternate by epoch parity so a rank one launch ahead never overwrites
 // messages a slower peer has not read yet

@@ -71,6 +71,12 @@ constexpr int kRD = 4;                      // depth of the per-row partial / sc
 // of its partner's mailbox reads, so 16 can never be overrun.
 constexpr int kMailD = 16;
 static_assert(kMailD == kXpMailD, "peer mailbox ring depth must match the cluster mailbox ring");
+// XP sender credit: the sender posts row n only after its receiver finished
+// row n - kXpCredit. Then a rank posting row n into a peer's slot n % kMailD
+// implies that peer's receiver finished row n - 2*kXpCredit >= n - kMailD.
+constexpr int kXpCredit = 6;
+constexpr int kCredD = 8;
+static_assert(2 * kXpCredit <= kMailD && kXpCredit < kCredD, "credit bounds");
 
 // Per-row scalars computed once by the control warp and broadcast in smem.
 struct RowScal {
@@ -220,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t red_bar[kRD], red_free[kRD];
   __shared__ __align__(16) RowScal scal[kRD];
   __shared__ __align__(8) uint64_t scal_bar[kRD], scal_free[kRD];
+  __shared__ __align__(8) uint64_t rcv_done[kCredD];  // XP: receiver progress (sender credit)
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x;
@@ -254,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&scal_bar[i]), 1);   // lane 0 of the control warp that wrote it
       mbar_init(smem_u32(&scal_free[i]), kBW);  // lane 0 of each backward warp
     }
+    for (int i = 0; i < kCredD; ++i) mbar_init(smem_u32(&rcv_done[i]), 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(smem_u32(&tmem_base_sh), kTCols);
@@ -495,6 +503,138 @@ __global__ void __launch_bounds__(kThreads, 1)
     const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
     const bool leader = (crank == 0 && lane == 0);
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (XP) {
+      // Peer exchange: the latency of a cross-GPU round trip is several rows
+      // long, so sending and receiving are split. Warp 0 (sender) merges the
+      // forward partials and posts them to every rank's mailbox as soon as the
+      // row's forward is done; warp 1 (receiver) consumes the rows in order,
+      // merges the P partials in rank order and publishes the scalars. The
+      // sender stays at most kXpCredit rows ahead of the receiver, which with
+      // the same bound on every rank keeps any rank from overrunning a peer's
+      // kMailD-deep mailbox ring.
+      uint32_t nrow = 0;
+      float wn = 0.f, An = 0.f, oldn = 0.f, refn = 0.f;
+      int32_t yn = 0;
+      if (cid < a.T) {
+        wn = __ldg(a.w_tok + cid);
+        yn = __ldg(a.targets + cid);
+        if (ci == 1) {
+          An = __ldg(a.adv_tok + cid);
+          oldn = __ldg(a.old_logp + cid);
+          refn = __ldg(a.ref_logp + cid);
+        }
+      }
+      for (int64_t t = cid; t < a.T; t += ncl) {
+        const float w = wn, A = An, old = oldn, ref = refn;
+        const int32_t ycur = yn;
+        if (t + ncl < a.T) {
+          const int64_t tn = t + ncl;
+          wn = __ldg(a.w_tok + tn);
+          yn = __ldg(a.targets + tn);
+          if (ci == 1) {
+            An = __ldg(a.adv_tok + tn);
+            oldn = __ldg(a.old_logp + tn);
+            refn = __ldg(a.ref_logp + tn);
+          }
+        }
+        if (w == 0.f) {
+          if (leader && ci == 0) {
+            if (a.out_logp) a.out_logp[t] = 0.f;
+            if (a.out_entropy) a.out_entropy[t] = 0.f;
+          }
+          continue;
+        }
+        const uint32_t mb = nrow % kMailD;
+        const uint64_t tag = static_cast<uint64_t>(static_cast<uint32_t>(a.xp_epoch << 20) + nrow + 1u) << 32;
+        const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
+        if (ci == 0) {
+          // ------------------------------------------------ sender
+          const uint32_t rs = nrow % kRD;
+          float zy = __int_as_float(0x7fc00000);
+          if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
+          if (nrow >= static_cast<uint32_t>(kXpCredit)) {
+            const uint32_t m = nrow - kXpCredit;
+            mbar_wait(smem_u32(&rcv_done[m % kCredD]), (m / kCredD) & 1u);
+          }
+          DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u));
+          Stats v = stats_empty();
+          if (lane < kFW) {
+            const float4 r = red[rs][lane];
+            v = Stats{r.x, r.y, r.z};
+          }
+          v = warp_merge(v);
+          if (lane == 0) mbar_arrive(smem_u32(&red_free[rs]));
+          if (lane < a.xp_P) {
+            XpMsg* dst = static_cast<XpMsg*>(a.xp_mail[lane]) + xp_index(a.xp_epoch, static_cast<int>(cid), mb, a.xp_rank);
+            st_sys_v2u64(&dst->w[0], tag | __float_as_uint(v.m2), tag | __float_as_uint(v.s));
+            st_sys_v2u64(&dst->w[2], tag | __float_as_uint(v.w), tag | __float_as_uint(zy));
+          }
+        } else {
+          // ------------------------------------------------ receiver
+          const uint32_t rs = nrow % kRD;
+          const uint32_t rpar = (nrow / kRD) & 1u;
+          const int64_t yl64 = yg - slice_start;
+          float4 mv = make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fc00000));
+          if (lane < a.xp_P) {
+            const XpMsg* src = static_cast<const XpMsg*>(a.xp_mail[a.xp_rank]) +
+                               xp_index(a.xp_epoch, static_cast<int>(cid), mb, lane);
+            constexpr uint64_t kHi = 0xffffffff00000000ull;
+            uint64_t q0, q1, q2, q3;
+            ld_sys_v2u64(&src->w[0], q0, q1);
+            ld_sys_v2u64(&src->w[2], q2, q3);
+            if (((q0 & kHi) != tag) | ((q1 & kHi) != tag) | ((q2 & kHi) != tag) | ((q3 & kHi) != tag)) {
+              const uint64_t t0 = globaltimer_ns();
+              do {
+                __nanosleep(64);
+                if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a peer never launched
+                  if (a.xp_err) atomicExch(a.xp_err, 1);
+                  __trap();
+                }
+                ld_sys_v2u64(&src->w[0], q0, q1);
+                ld_sys_v2u64(&src->w[2], q2, q3);
+              } while (((q0 & kHi) != tag) | ((q1 & kHi) != tag) | ((q2 & kHi) != tag) | ((q3 & kHi) != tag));
+            }
+            mv = make_float4(__uint_as_float(static_cast<uint32_t>(q0)), __uint_as_float(static_cast<uint32_t>(q1)),
+                             __uint_as_float(static_cast<uint32_t>(q2)), __uint_as_float(static_cast<uint32_t>(q3)));
+          }
+          // merge in rank order (identical scalars on every rank); the owner's z_target
+          Stats st = stats_empty();
+          float zy = __int_as_float(0x7fc00000);
+          for (int q = 0; q < a.xp_P; ++q) {
+            const float zq = __shfl_sync(0xffffffffu, mv.w, q);
+            st = stats_merge(st, Stats{__shfl_sync(0xffffffffu, mv.x, q), __shfl_sync(0xffffffffu, mv.y, q),
+                                       __shfl_sync(0xffffffffu, mv.z, q)});
+            if (zq == zq) zy = zq;
+          }
+          float lse2, lse, H, logp;
+          row_scalars(st, zy, lse2, lse, H, logp);
+          float g, gH, m[8];
+          loss_terms(logp, H, w, A, old, ref, P, g, gH, m);
+          if (leader) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(m[i]);
+            if (a.out_logp) a.out_logp[t] = logp;
+            if (a.out_entropy) a.out_entropy[t] = H;
+          }
+          if (lane == 0) {
+            RowScal r;
+            r.lse2 = lse2;
+            r.gt = a.inv_tau * g;
+            r.c0 = a.inv_tau * (g + gH * H);
+            r.c1 = a.inv_tau * gH * kLn2;
+            r.lse2f = lse2 - log2f(fabsf(r.c0));
+            r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
+            r.yl = (yl64 >= 0 && yl64 < slice_len) ? static_cast<int>(yl64) : -1;
+            r.pad = 0.f;
+            mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
+            scal[rs] = r;
+            mbar_arrive(smem_u32(&scal_bar[rs]));
+            mbar_arrive(smem_u32(&rcv_done[nrow % kCredD]));  // the shuffles consumed the messages
+          }
+        }
+        ++nrow;
+      }
+    } else {
     uint32_t nrow = 0;
     float wn = 0.f, An = 0.f, oldn = 0.f, refn = 0.f;
     int32_t yn = 0;
@@ -547,39 +687,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float z = 0.f;
       const uint32_t mb = nrow % kMailD;
       Stats st = stats_empty();
-      if constexpr (XP) {
-        // lane q posts this rank's partial into rank q's mailbox (q == own rank:
-        // local), then polls the message from rank q in its own mailbox
-        const unsigned long long tag = (a.xp_epoch << 32) | static_cast<unsigned long long>(nrow + 1);
-        float4 mv = make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fc00000));
-        if (lane < a.xp_P) {
-          XpMsg* dst = static_cast<XpMsg*>(a.xp_mail[lane]) + xp_index(a.xp_epoch, static_cast<int>(cid), mb, a.xp_rank);
-          st_sys_v4(dst->v, v.m2, v.s, v.w, zy);
-          st_release_sys_u64(&dst->tag, tag);
-          const XpMsg* src = static_cast<const XpMsg*>(a.xp_mail[a.xp_rank]) +
-                             xp_index(a.xp_epoch, static_cast<int>(cid), mb, lane);
-          if (ld_acquire_sys_u64(&src->tag) != tag) {
-            const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_sys_u64(&src->tag) != tag) {
-              __nanosleep(200);
-              if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a peer never launched
-                if (a.xp_err) atomicExch(a.xp_err, 1);
-                __trap();
-              }
-            }
-          }
-          mv = ld_sys_v4(src->v);
-        }
-        // merge in rank order (identical scalars on every rank); the owner's z_target
-        for (int q = 0; q < a.xp_P; ++q) {
-          const float m2q = __shfl_sync(0xffffffffu, mv.x, q);
-          const float sq = __shfl_sync(0xffffffffu, mv.y, q);
-          const float wq = __shfl_sync(0xffffffffu, mv.z, q);
-          const float zq = __shfl_sync(0xffffffffu, mv.w, q);
-          st = stats_merge(st, Stats{m2q, sq, wq});
-          if (zq == zq) zy = zq;
-        }
-      } else {
       if (lane == 0) {
         if (C == 1) {
           mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
@@ -604,7 +711,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float4 mv = mail[mb][q];
         st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
       }
-      }  // !XP
       float lse2, lse, H, logp;
       row_scalars(st, zy, lse2, lse, H, logp);
       float g, gH, m[8];
@@ -636,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     
       ++nrow;
     }
+    }  // XP / alternating
     // fixed-order combine of the two control warps' fp64 partials, then the
     // deterministic cross-block finish
     __shared__ double acc_sh[8];
