@@ -38,6 +38,9 @@ def launches(tag):
     allns = sum(tot.values())
     md = [f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 1`",
           "", "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400` (cold-cache, serialised: compare shares).",
+          "The whole program is listed: `synth_logits_kernel` and the 16 `rows_ring_kernel<.., 0, 2>` launches "
+          "(behaviour/reference log-probs of the synthetic batch) are setup outside the timed region; inside it "
+          "the fused kernel is 99.9% of the step (`kernel_share_of_step` in the bench line).",
           "", "| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         md.append(f"| `{k}` | {cnt[k]} | {v / 1e6:.3f} | {v / allns * 100:.2f}% |")
