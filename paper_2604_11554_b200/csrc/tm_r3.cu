@@ -292,11 +292,13 @@ __global__ void __launch_bounds__(256)
   uint32_t cur_cnt = 0;
   // rows of the next pair are loaded one iteration ahead (two pairs in flight per warp)
   float zn[NB][4];
+  int en = -1;  // next pair's recorded expert of this lane, prefetched with its logits
   if (p0 < p1) {
     const int64_t r = 2 * p0 + (lane >> 4);
     const int64_t rc = r < rows ? r : rows - 1;
 #pragma unroll
     for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+    if (gl < k) en = r3_idx(rec, idx_dtype, rc * k + gl);
   }
   for (int64_t pr = p0; pr < p1; ++pr) {
     const int64_t row = 2 * pr + (lane >> 4);
@@ -307,26 +309,18 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < NB; ++i)
 #pragma unroll
       for (int c = 0; c < 4; ++c) z[i][c] = zn[i][c];
+    const int my_e = en;
     if (pr + 1 < p1) {
       const int64_t r = 2 * (pr + 1) + (lane >> 4);
       const int64_t rc = r < rows ? r : rows - 1;
 #pragma unroll
       for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+      if (gl < k) en = r3_idx(rec, idx_dtype, rc * k + gl);
     }
-    int my_e = -1;
     float zr = -INFINITY;
     if (gl < k) {
-      my_e = r3_idx(rec, idx_dtype, rowc * k + gl);
+      // the recorded logit: an L1 hit (the row's lines were loaded one iteration ago)
       zr = (my_e >= 0 && my_e < E) ? r3_load(logits, rowc * E + my_e) : __int_as_float(0x7fc00000);
-    }
-    // membership of my experts in the recorded set (k <= 16, unrolled)
-    uint32_t mine = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j < k) {
-        const int e = __shfl_sync(0xffffffffu, my_e, j, kG);
-        if (e >= 0 && e < E && ((e & 63) >> 2) == gl) mine |= 1u << ((e >> 6) * 4 + (e & 3));
-      }
     }
     // gate weights
     float wj;
@@ -353,25 +347,49 @@ __global__ void __launch_bounds__(256)
       if (out_idx) out_idx[row * k + gl] = my_e;
     }
     if (mismatch) {
-      // worst recorded vs best non-recorded logit; exact index tie-break (P9) only on equality
-      float in_min = INFINITY, out_max = -INFINITY;
+      // Recorded set R (k distinct valid experts) equals the trainer's top-k iff no
+      // expert outside R beats in_min = min over R under (logit desc, index asc).
+      // Counting the experts above / equal to in_min decides it without knowing
+      // which lane holds which recorded expert; only an exact tie at in_min with
+      // a non-recorded expert needs the per-expert membership (rare slow path).
+      const bool bad_e = gl < k && !(my_e >= 0 && my_e < E);
+      const unsigned key = (gl < k && !bad_e) ? ((static_cast<unsigned>(lane >> 4) << 16) | static_cast<unsigned>(my_e))
+                                              : (0x80000000u | static_cast<unsigned>(lane));
+      const unsigned same = __match_any_sync(0xffffffffu, key);  // every lane (no short-circuit)
+      const bool dup = gl < k && __popc(same) > 1;
+      const unsigned badb = __ballot_sync(0xffffffffu, bad_e || dup);
+      const bool grp_bad = ((badb >> (lane & 16)) & 0xffffu) != 0u;
+      float in_min = (gl < k && !bad_e) ? zr : INFINITY;
+#pragma unroll
+      for (int o = kG / 2; o > 0; o >>= 1) in_min = fminf(in_min, __shfl_xor_sync(0xffffffffu, in_min, o, kG));
+      // all k recorded experts are >= in_min: any further expert >= in_min is either
+      // a mismatch or an exact tie, both settled below on the (rare) slow path
+      int n_ge = 0;
 #pragma unroll
       for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const bool rin = (mine >> (i * 4 + c)) & 1u;
-          in_min = rin ? fminf(in_min, z[i][c]) : in_min;
-          out_max = rin ? out_max : fmaxf(out_max, z[i][c]);
-        }
+        for (int c = 0; c < 4; ++c) n_ge += z[i][c] >= in_min ? 1 : 0;
+      n_ge = gsumi(n_ge);
+      bool mm = grp_bad;
+      const bool slow = !grp_bad && n_ge > k;
+      if (__any_sync(0xffffffffu, slow)) {
+        // membership of my experts in the recorded set (k <= 16, unrolled)
+        uint32_t mine = 0;
 #pragma unroll
-      for (int o = kG / 2; o > 0; o >>= 1) {
-        in_min = fminf(in_min, __shfl_xor_sync(0xffffffffu, in_min, o, kG));
-        out_max = fmaxf(out_max, __shfl_xor_sync(0xffffffffu, out_max, o, kG));
-      }
-      const int distinct = gsumi(__popc(mine));
-      bool mm = (distinct != k) || (out_max > in_min);
-      if (__any_sync(0xffffffffu, out_max == in_min)) {
-        // tie: the trainer prefers the lower index among equal logits
+        for (int j = 0; j < 16; ++j) {
+          if (j < k) {
+            const int e = __shfl_sync(0xffffffffu, my_e, j, kG);
+            if (e >= 0 && e < E && ((e & 63) >> 2) == gl) mine |= 1u << ((e >> 6) * 4 + (e & 3));
+          }
+        }
+        // best non-recorded logit; on an exact tie the trainer prefers the lower index
+        float out_max = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (!((mine >> (i * 4 + c)) & 1u)) out_max = fmaxf(out_max, z[i][c]);
+        out_max = gmaxf(out_max);
         int in_hi = -1, out_lo = 0x7fffffff;
 #pragma unroll
         for (int i = 0; i < NB; ++i)
@@ -380,31 +398,35 @@ __global__ void __launch_bounds__(256)
             const int e = i * 64 + 4 * gl + c;
             const bool rin = (mine >> (i * 4 + c)) & 1u;
             if (rin && z[i][c] == in_min) in_hi = max(in_hi, e);
-            if (!rin && z[i][c] == out_max) out_lo = min(out_lo, e);
+            if (!rin && z[i][c] == in_min) out_lo = min(out_lo, e);
           }
 #pragma unroll
         for (int o = kG / 2; o > 0; o >>= 1) {
           in_hi = max(in_hi, __shfl_xor_sync(0xffffffffu, in_hi, o, kG));
           out_lo = min(out_lo, __shfl_xor_sync(0xffffffffu, out_lo, o, kG));
         }
-        if (out_max == in_min && out_lo < in_hi) mm = true;
+        if (slow && (out_max > in_min || (out_max == in_min && out_lo < in_hi))) mm = true;
       }
       // per-layer counts; the layer boundary advances incrementally (no 64-bit division per row)
       const unsigned bal = __ballot_sync(0xffffffffu, valid && mm && gl == 0);
+      if (2 * pr + 1 < layer_end && 2 * pr + 1 < rows) {
+        cur_cnt += __popc(bal & 0x00010001u);  // both rows of the pair in the current layer
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t rr = 2 * pr + h;
-        if (rr >= rows) continue;
-        if (rr >= layer_end) {
-          if (cur_cnt && lane == 0) {
-            atomicAdd(mismatch + cur_layer, cur_cnt);
-            atomicAdd(mismatch + L, cur_cnt);
+        for (int h = 0; h < 2; ++h) {
+          const int64_t rr = 2 * pr + h;
+          if (rr >= rows) continue;
+          if (rr >= layer_end) {
+            if (cur_cnt && lane == 0) {
+              atomicAdd(mismatch + cur_layer, cur_cnt);
+              atomicAdd(mismatch + L, cur_cnt);
+            }
+            cur_layer = rr / Tn;
+            layer_end = (cur_layer + 1) * Tn;
+            cur_cnt = 0;
           }
-          cur_layer = rr / Tn;
-          layer_end = (cur_layer + 1) * Tn;
-          cur_cnt = 0;
+          if ((bal >> (h * 16)) & 1u) ++cur_cnt;
         }
-        if ((bal >> (h * 16)) & 1u) ++cur_cnt;
       }
     }
   }
@@ -426,16 +448,25 @@ __global__ void __launch_bounds__(256)
   float* rb = buf[threadIdx.x >> 5][half];
   const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // the next pair's (index, w, dw) are loaded one iteration ahead
+  int en = -1;
+  float wn = 0.f, dwn = 0.f;
+  if (2 * gw < rows && gl < k) {
+    const int64_t r = 2 * gw + half < rows ? 2 * gw + half : rows - 1;
+    en = r3_idx(rec, idx_dtype, r * k + gl);
+    wn = w[r * k + gl];
+    dwn = dw[r * k + gl];
+  }
   for (int64_t pr = gw; 2 * pr < rows; pr += nw) {
     const int64_t row = 2 * pr + half;
     const bool valid = row < rows;
-    const int64_t rowc = valid ? row : rows - 1;
-    int my_e = -1;
-    float wj = 0.f, dwj = 0.f;
-    if (gl < k) {
-      my_e = r3_idx(rec, idx_dtype, rowc * k + gl);
-      wj = w[rowc * k + gl];
-      dwj = dw[rowc * k + gl];
+    const int my_e = en;
+    const float wj = wn, dwj = dwn;
+    if (2 * (pr + nw) < rows && gl < k) {
+      const int64_t r = 2 * (pr + nw) + half < rows ? 2 * (pr + nw) + half : rows - 1;
+      en = r3_idx(rec, idx_dtype, r * k + gl);
+      wn = w[r * k + gl];
+      dwn = dw[r * k + gl];
     }
     const float S = gsumf(wj * dwj);
 #pragma unroll

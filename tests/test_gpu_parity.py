@@ -369,13 +369,15 @@ def test_r3_gate(tm, orc, dtype, idx_dtype, renorm):
     for l, t in zip(*np.nonzero(flip)):
         others = np.setdiff1d(np.arange(E), rec[l, t])
         rec[l, t, rng.integers(0, k)] = rng.choice(others)
+    rec[2, :4, 1] = rec[2, :4, 0]  # duplicated recorded expert: not a top-k set (mismatch)
+    rec[1, 3:6] = order[1, 3:6, 1:k + 1]  # shifted by one: a boundary swap
     rec = rec.astype(np.uint8 if idx_dtype == "u8" else np.int32)
     rt = torch.from_numpy(rec).cuda()
     w, idx, mm = tm.r3_gate_fwd(zt, rt, renorm=renorm)
     ow, oidx, omm = orc.r3_gate_fwd(zin, rec, renorm=renorm)
     assert orc.digest(idx.cpu().numpy()) == orc.digest(oidx)  # replayed indices bit-exact
     assert np.array_equal(mm.cpu().numpy().astype(np.uint32), omm)
-    assert omm[L] == flip.sum()
+    assert omm[L] >= flip.sum()
     assert_close(w.cpu().numpy(), ow, atol=1e-6, rtol=1e-5, what="r3 w")
     dw = rng.normal(size=(L, T, k)).astype(np.float32)
     wg = w.cpu().numpy()
