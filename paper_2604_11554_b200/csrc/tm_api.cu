@@ -641,8 +641,8 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
   if (ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= Vp");
   const int64_t es = dtype == SF_TM_BF16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(logits_shard) | reinterpret_cast<uintptr_t>(dlogits)) % 16 ||
-      (ld * es) % 16 || (ld_d * es) % 16)
-    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows and strides");
+      (ld * es) % 16 || (ld_d * es) % 16 || (Vp * es) % 16)
+    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows, widths and strides");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ++h->xp_epoch;  // every rank calls in the same order, so epochs agree
   if (T == 0) {

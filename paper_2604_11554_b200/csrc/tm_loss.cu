@@ -408,13 +408,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
           }
         } else {
+          // Partial chunk. Slice lengths are multiples of the 16-B vector (the
+          // ring path requires it), so each of this thread's two vectors lies
+          // wholly inside or outside the slice: the packed path, per vector.
+          // A -inf logit makes w NaN here as on full chunks -> row-end repair.
+          const bool ok0 = EV * ftid < rem, ok1 = G::HALF + EV * ftid < rem;
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
 #pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
-              const float av = fmaf(x[j], c, -m2);
-              const float e = ex2(av);
-              s2[0].x += e;
-              w2[0].x = fmaf(e, av, w2[0].x);
+          for (int p = 0; p < NE / 2; ++p) {
+            if ((2 * p < EV) ? ok0 : ok1) {
+              const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
+              const float2 e = make_float2(ex2(av.x), ex2(av.y));
+              s2[p & 1] = __fadd2_rn(s2[p & 1], e);
+              w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
             }
           }
         }
@@ -826,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
         T* dst = drow + k * CE;
+        const int rem = slice_len - k * CE;
         if (!partial && (dbg_mode & 2)) {  // debug: store the words back (pipeline ceiling)
           if (!(dbg_mode & 4)) {
             stg128_cs(dst + EV * btid, w0);
@@ -852,23 +859,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < NE; ++j)
               if (j == jt) gr[j] += gts;
           }
+          uint4 p0, p1;
+          p0.x = pack_bf16x2(gr[0], gr[1]) ^ sgn;
+          p0.y = pack_bf16x2(gr[2], gr[3]) ^ sgn;
+          p0.z = pack_bf16x2(gr[4], gr[5]) ^ sgn;
+          p0.w = pack_bf16x2(gr[6], gr[7]) ^ sgn;
+          p1.x = pack_bf16x2(gr[8], gr[9]) ^ sgn;
+          p1.y = pack_bf16x2(gr[10], gr[11]) ^ sgn;
+          p1.z = pack_bf16x2(gr[12], gr[13]) ^ sgn;
+          p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
           if (!partial) {
-            uint4 p0, p1;
-            p0.x = pack_bf16x2(gr[0], gr[1]) ^ sgn;
-            p0.y = pack_bf16x2(gr[2], gr[3]) ^ sgn;
-            p0.z = pack_bf16x2(gr[4], gr[5]) ^ sgn;
-            p0.w = pack_bf16x2(gr[6], gr[7]) ^ sgn;
-            p1.x = pack_bf16x2(gr[8], gr[9]) ^ sgn;
-            p1.y = pack_bf16x2(gr[10], gr[11]) ^ sgn;
-            p1.z = pack_bf16x2(gr[12], gr[13]) ^ sgn;
-            p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
             stg128_cs(dst + EV * btid, p0);
             stg128_cs(dst + G::HALF + EV * btid, p1);
-            if (late) mbar_arrive(rel);
-            return;
+          } else {
+            // vector-granular tail (see the forward's partial chunk)
+            if (EV * btid < rem) stg128_cs(dst + EV * btid, p0);
+            if (G::HALF + EV * btid < rem) stg128_cs(dst + G::HALF + EV * btid, p1);
+            __threadfence_block();  // a thread may store nothing: order the LDS before the release
           }
-#pragma unroll
-          for (int j = 0; j < NE; ++j) gr[j] = neg ? -gr[j] : gr[j];
+          if (late) mbar_arrive(rel);
+          return;
         } else if (mode == 1) {
           const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2, -lse2);
           const float2 mc0 = make_float2(-c0, -c0);
@@ -900,13 +910,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_vec(dst + EV * btid, gr);
           store_vec(dst + G::HALF + EV * btid, gr + EV);
         } else {
-          const int rem = slice_len - k * CE;
-#pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const int off = elem_off<T>(btid, j);
-            if (off < rem) st1(dst + off, gr[j]);
-          }
-          __threadfence_block();  // the masked tail may store nothing: order the LDS before the release
+          if (EV * btid < rem) store_vec(dst + EV * btid, gr);
+          if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
+          __threadfence_block();  // a thread may store nothing: order the LDS before the release
         }
         if (late) mbar_arrive(rel);
       };
