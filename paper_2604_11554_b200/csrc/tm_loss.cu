@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t scal_bar[kRD], scal_free[kRD];
   __shared__ __align__(8) uint64_t rcv_done[kCredD];  // XP: receiver progress (sender credit)
   __shared__ uint32_t tmem_base_sh;
+  __shared__ uint32_t sink_sh[kBW];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -772,6 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
     const uint32_t tm_t = tbase + tlane + tcol;
     const uint32_t stash_t = stash_base + 16u * btid;
+    const uint32_t sink_a = smem_u32(&sink_sh[warp]);  // dummy-store target (never read)
     uint32_t ts = 0, tph = 0, nrow = 0;
     float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
     for (int64_t t = cid; t < a.T; t += ncl) {
@@ -873,9 +875,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             stg128_cs(dst + G::HALF + EV * btid, p1);
           } else {
             // vector-granular tail (see the forward's partial chunk)
-            if (EV * btid < rem) stg128_cs(dst + EV * btid, p0);
-            if (G::HALF + EV * btid < rem) stg128_cs(dst + G::HALF + EV * btid, p1);
-            __threadfence_block();  // a thread may store nothing: order the LDS before the release
+            const bool s0 = EV * btid < rem, s1 = G::HALF + EV * btid < rem;
+            if (s0) stg128_cs(dst + EV * btid, p0);
+            if (s1) stg128_cs(dst + G::HALF + EV * btid, p1);
+            // a thread storing nothing still orders its loads before the
+            // releases below through a dependent (dummy) smem store
+            if (!s0) sink_u32(sink_a, p0.x ^ p1.y);
           }
           if (late) mbar_arrive(rel);
           return;
@@ -910,9 +915,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_vec(dst + EV * btid, gr);
           store_vec(dst + G::HALF + EV * btid, gr + EV);
         } else {
-          if (EV * btid < rem) store_vec(dst + EV * btid, gr);
+          const bool s0 = EV * btid < rem;
+          if (s0) store_vec(dst + EV * btid, gr);
           if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
-          __threadfence_block();  // a thread may store nothing: order the LDS before the release
+          if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]));
         }
         if (late) mbar_arrive(rel);
       };
@@ -927,9 +933,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < nfull; ++k) bchunk(k, false, 2);
         if (nck > nfull) bchunk(nfull, true, 2);
       }
-      // the row's stores consumed every lane's scalars (the fence covers rows
-      // with nothing to store): free the scal slot
-      __threadfence_block();
+      // the row's stores consumed every lane's scalars (a row with no chunk
+      // here consumes them through a dependent dummy smem store): free the slot
+      if (nck == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.yl);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;

@@ -1,4 +1,4 @@
 #!/bin/bash
 touch paper_2604_11554_b200/csrc/tm_loss.cu
 make -s -j8 -C paper_2604_11554_b200/csrc EXTRA=-DSFTM_WAIT_PROFILE > /dev/null 2>&1 || exit 1
-for C in ${CS:-0}; do echo "== C=$C"; SFTM_LOSS_C=$C python scripts/wait_profile.py; done
+for V in ${VS:-151936}; do for C in ${CS:-0}; do echo "== V=$V C=$C"; SFTM_LOSS_C=$C python scripts/wait_profile.py ${ROWS:-32768} $V; done; done
