@@ -318,16 +318,27 @@ __device__ __forceinline__ Stats stats_merge(Stats a, Stats b) {
   return r;
 }
 
+// Warp-wide merge: the max first, then every lane rescales its own partial to
+// it once (one ex2) and s, w are summed — 15 shuffles and 1 ex2 per lane
+// instead of 5 pairwise merges with 2 ex2 each. Fixed butterfly order, so the
+// result is deterministic.
 __device__ __forceinline__ Stats warp_merge(Stats v) {
+  float M = v.m2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float s = 0.f, w = 0.f;
+  if (v.m2 != -INFINITY) {
+    const float d = v.m2 - M;
+    const float f = ex2(d);
+    s = v.s * f;
+    w = f * fmaf(v.s, d, v.w);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    Stats u;
-    u.m2 = __shfl_xor_sync(0xffffffffu, v.m2, o);
-    u.s = __shfl_xor_sync(0xffffffffu, v.s, o);
-    u.w = __shfl_xor_sync(0xffffffffu, v.w, o);
-    v = stats_merge(v, u);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    w += __shfl_xor_sync(0xffffffffu, w, o);
   }
-  return v;
+  return Stats{M, s, w};
 }
 
 }  // namespace sftm

@@ -3,6 +3,7 @@
 // reads) reach the bandwidth of a grid-stride copy?
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2604_11554_b200/csrc -o scripts/mb_copy scripts/microbench_copy.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "tm_device.cuh"
@@ -90,8 +91,9 @@ __global__ void ldg_copy(const uint4* src, uint4* dst, size_t n16) {
     __stcs(dst + i, __ldcs(src + i));
 }
 
-int main() {
-  const size_t row_bytes = 151936 * 2 / 2;  // one CTA's half row at C=2 (bf16)
+int main(int argc, char** argv) {
+  // default: one CTA's half row at C=2 (bf16); argv[1] overrides (bytes)
+  const size_t row_bytes = argc > 1 ? static_cast<size_t>(atol(argv[1])) : size_t(151936) * 2 / 2;
   const size_t rows = (size_t(16) << 30) / row_bytes;
   const size_t bytes = rows * row_bytes;
   char *src, *dst;
@@ -121,8 +123,8 @@ int main() {
                 {8192, 26, 0, 0, "TMA ring -> STG same chunk"},
                 {12288, 17, 1, 0, "TMA ring -> TMA bulk store"},
                 {8192, 26, 1, 0, "TMA ring -> TMA bulk store"},
-                {12288, 17, 2, 13, "TMA ring -> STG lag 1 row"},
-                {12288, 17, 2, 26, "TMA ring -> STG lag 2 rows"}};
+                {12288, 17, 2, static_cast<int>(row_bytes / 12288), "TMA ring -> STG lag 1 row"},
+                {12288, 17, 2, static_cast<int>(2 * (row_bytes / 12288)), "TMA ring -> STG lag 2 rows"}};
   for (auto c : cfgs) {
     const size_t rb = row_bytes / c.chunk * c.chunk;
     const size_t nrows = bytes / rb;
