@@ -22,10 +22,17 @@
 //                            field: GRPO is then computed here over `group`)
 //   loss_mask  uint8[L_i]    optional; default all ones
 //   group      int32         optional group id; default (sample_id-1)/group_size
+//   routed_experts uint8[L_i * layers * k]  R3 record, token-major (token, layer, slot);
+//                            decoded by pack_routed_experts into the gate's
+//                            layer-major [layers, T, k] operand
+// Staleness tags pass through from MicroBatch.producer_versions:
+// staleness = v_trainer - v_producer per sample, as StalenessGate::staleness_of
+// (proj/src/staleness.cpp:169-173) defines it for the batch minimum.
 #pragma once
 
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -44,7 +51,37 @@ struct PackedBatch {
   std::vector<int32_t> seq_lens, group_ids;
   std::vector<float> per_sample;  // advantages, or rewards when !has_advantage
   bool has_advantage = false;
+  std::vector<int64_t> producer_versions;  // per sample (MicroBatch.producer_versions)
 };
+
+// Per-sample staleness histogram {v_trainer - v_producer: count} and the batch
+// staleness v_trainer - min(v_producer) (StalenessGate::staleness_of).
+inline std::map<int64_t, uint64_t> staleness_histogram(const PackedBatch& p, int64_t v_trainer,
+                                                       int64_t* batch_staleness = nullptr) {
+  std::map<int64_t, uint64_t> h;
+  int64_t vmin = v_trainer;
+  for (int64_t v : p.producer_versions) {
+    ++h[v_trainer - v];
+    if (v < vmin) vmin = v;
+  }
+  if (batch_staleness) *batch_staleness = v_trainer - vmin;
+  return h;
+}
+
+// GRPO is only correct on complete groups: every group id of the
+// batch must occur exactly group_size times. SF_TM_OK or SF_TM_CONFIG_ERROR.
+inline int check_complete_groups(const PackedBatch& p, int group_size, std::string* err) {
+  if (group_size <= 0) return SF_TM_OK;
+  std::map<int32_t, int> n;
+  for (int32_t g : p.group_ids) ++n[g];
+  for (const auto& kv : n)
+    if (kv.second != group_size) {
+      if (err) *err = "group " + std::to_string(kv.first) + " has " + std::to_string(kv.second) + " of " +
+                      std::to_string(group_size) + " samples in this micro-batch";
+      return SF_TM_CONFIG_ERROR;
+    }
+  return SF_TM_OK;
+}
 
 namespace detail {
 inline int find_field(const std::vector<std::string>& fs, const char* name) {
@@ -107,6 +144,49 @@ int pack_trainer_batch(const MicroBatchT& b, int group_size, PackedBatch& out, s
     out.seq_lens.push_back(static_cast<int32_t>(L));
     out.T += static_cast<int64_t>(L);
   }
+  if (b.producer_versions.size() == b.sample_ids.size())
+    out.producer_versions.assign(b.producer_versions.begin(), b.producer_versions.end());
+  return SF_TM_OK;
+}
+
+// Decode the "routed_experts" field of every sample into the R3 gate's recorded
+// index operand, layer-major uint8 [layers, T, k] with T = sum of the samples'
+// response lengths in bus order (the same token order as pack_trainer_batch).
+// Returns SF_TM_OK or SF_TM_CONFIG_ERROR (missing field, size not L_i*layers*k).
+template <class MicroBatchT>
+int pack_routed_experts(const MicroBatchT& b, int layers, int k, std::vector<uint8_t>& out, int64_t* T_out,
+                        std::string* err) {
+  const int jr = detail::find_field(b.field_set, "response");
+  const int je = detail::find_field(b.field_set, "routed_experts");
+  if (jr < 0 || je < 0 || layers <= 0 || k <= 0) {
+    if (err) *err = "routed_experts needs the response and routed_experts fields and layers, k > 0";
+    return SF_TM_CONFIG_ERROR;
+  }
+  if (b.payloads.size() != b.sample_ids.size()) {
+    if (err) *err = "payloads missing (fetch with with_payload=true)";
+    return SF_TM_CONFIG_ERROR;
+  }
+  int64_t T = 0;
+  for (size_t i = 0; i < b.payloads.size(); ++i) {
+    const size_t L = b.payloads[i][jr].size() / sizeof(int32_t);
+    if (b.payloads[i][je].size() != L * static_cast<size_t>(layers) * k) {
+      if (err) *err = "sample " + std::to_string(b.sample_ids[i]) + ": routed_experts is not L*layers*k bytes";
+      return SF_TM_CONFIG_ERROR;
+    }
+    T += static_cast<int64_t>(L);
+  }
+  out.assign(static_cast<size_t>(layers) * T * k, 0);
+  int64_t t0 = 0;
+  for (size_t i = 0; i < b.payloads.size(); ++i) {
+    const auto& src = b.payloads[i][je];
+    const int64_t L = static_cast<int64_t>(b.payloads[i][jr].size() / sizeof(int32_t));
+    for (int64_t t = 0; t < L; ++t)
+      for (int l = 0; l < layers; ++l)
+        std::memcpy(out.data() + ((static_cast<size_t>(l) * T + t0 + t) * k),
+                    src.data() + ((static_cast<size_t>(t) * layers + l) * k), static_cast<size_t>(k));
+    t0 += L;
+  }
+  if (T_out) *T_out = T;
   return SF_TM_OK;
 }
 
@@ -127,14 +207,18 @@ class ActorLossSeam {
 
   // Decode `batch`, copy its bus fields through pinned staging, and run the
   // fused DAPO/GRPO loss fwd+bwd on `d_logits` [T, V] (row stride V). Writes
-  // dlogits and the metrics (valid once `stream` is synchronised).
+  // dlogits and the metrics (valid once `stream` is synchronised). When the
+  // batch carries rewards (GRPO computed here), every group must be complete
+  // in the micro-batch unless allow_partial_groups.
   template <class MicroBatchT>
   int step(const MicroBatchT& batch, const void* d_logits, int32_t dtype, int64_t V, void* d_dlogits,
            const sf_tm_loss_params& params, float* h_metrics, void* stream, int group_size = 0,
-           float adv_eps = 1e-6f, int32_t std_mode = SF_TM_STD_UNBIASED) {
+           float adv_eps = 1e-6f, int32_t std_mode = SF_TM_STD_UNBIASED, bool allow_partial_groups = false) {
     if (rc_ != SF_TM_OK) return rc_;
     std::string err;
     int rc = pack_trainer_batch(batch, group_size, packed_, &err);
+    if (rc == SF_TM_OK && !packed_.has_advantage && !allow_partial_groups)
+      rc = check_complete_groups(packed_, group_size, &err);
     if (rc != SF_TM_OK) {
       err_ = err;
       return rc;

@@ -69,7 +69,7 @@ MicroBatch make_batch(int V, int S, int Lmax, unsigned seed, bool with_adv) {
     }
     const float reward = (rnd() % 2) ? 1.f : 0.f, adv = ((rnd() % 200) - 100) * 1e-2f;
     b.sample_ids.push_back(static_cast<std::uint64_t>(i + 1));
-    b.producer_versions.push_back(3);
+    b.producer_versions.push_back(3 + (i % 2));
     b.global_steps.push_back(7);
     if (with_adv)
       b.payloads.push_back({enc(std::vector<float>{adv}), enc(lp), enc(rl), enc(resp), enc(std::vector<float>{reward})});
@@ -107,6 +107,53 @@ void test_pack() {
   CHECK(staleflow::train_math::pack_trainer_batch(r, 4, p, &err) == SF_TM_CONFIG_ERROR && !err.empty());
   r.field_set = {"logp", "response"};
   CHECK(staleflow::train_math::pack_trainer_batch(r, 4, p, &err) == SF_TM_CONFIG_ERROR);
+  // staleness tags pass through: v_t - v_producer per sample, batch = v_t - min
+  MicroBatch st = make_batch(1000, 6, 20, 3, true);
+  CHECK(staleflow::train_math::pack_trainer_batch(st, 0, p, &err) == SF_TM_OK);
+  int64_t bs = -1;
+  auto hist = staleflow::train_math::staleness_histogram(p, 5, &bs);
+  CHECK(bs == 2 && hist.size() == 2 && hist[2] == 3 && hist[1] == 3);
+  // complete groups (H6): 8 samples in groups of 4 pass; dropping one fails
+  MicroBatch g = make_batch(1000, 8, 20, 5, false);
+  CHECK(staleflow::train_math::pack_trainer_batch(g, 4, p, &err) == SF_TM_OK);
+  CHECK(staleflow::train_math::check_complete_groups(p, 4, &err) == SF_TM_OK);
+  g.sample_ids.pop_back();
+  g.payloads.pop_back();
+  g.producer_versions.pop_back();
+  g.global_steps.pop_back();
+  CHECK(staleflow::train_math::pack_trainer_batch(g, 4, p, &err) == SF_TM_OK);
+  CHECK(staleflow::train_math::check_complete_groups(p, 4, &err) == SF_TM_CONFIG_ERROR && !err.empty());
+  // routed_experts: token-major (token, layer, slot) payloads -> layer-major [layers, T, k]
+  {
+    const int layers = 3, k = 2;
+    MicroBatch rb;
+    rb.field_set = {"response", "routed_experts"};
+    const int lens[2] = {4, 5};
+    for (int i = 0; i < 2; ++i) {
+      rb.sample_ids.push_back(static_cast<std::uint64_t>(i + 1));
+      rb.producer_versions.push_back(1);
+      rb.global_steps.push_back(1);
+      Bytes rec(static_cast<size_t>(lens[i]) * layers * k);
+      for (int t = 0; t < lens[i]; ++t)
+        for (int l = 0; l < layers; ++l)
+          for (int j = 0; j < k; ++j) rec[(t * layers + l) * k + j] = static_cast<std::uint8_t>(100 * i + 10 * t + 3 * l + j);
+      rb.payloads.push_back({enc(std::vector<int32_t>(lens[i], 7)), rec});
+    }
+    std::vector<uint8_t> lm;
+    int64_t T = 0;
+    CHECK(staleflow::train_math::pack_routed_experts(rb, layers, k, lm, &T, &err) == SF_TM_OK);
+    CHECK(T == 9 && lm.size() == static_cast<size_t>(layers * T * k));
+    bool ok = true;
+    for (int l = 0; l < layers; ++l)
+      for (int t = 0; t < 9; ++t)
+        for (int j = 0; j < k; ++j) {
+          const int i = t < 4 ? 0 : 1, tt = t < 4 ? t : t - 4;
+          ok &= lm[(static_cast<size_t>(l) * T + t) * k + j] == static_cast<std::uint8_t>(100 * i + 10 * tt + 3 * l + j);
+        }
+    CHECK(ok);
+    rb.payloads[1][1].pop_back();
+    CHECK(staleflow::train_math::pack_routed_experts(rb, layers, k, lm, &T, &err) == SF_TM_CONFIG_ERROR);
+  }
   std::printf(fails ? "PACK FAILED\n" : "PACK OK\n");
 }
 
@@ -143,6 +190,45 @@ void test_gpu() {
   cudaFree(logits);
   cudaFree(dl1);
   cudaFree(dl2);
+  // routed_experts codec -> R3 gate: the replayed indices are the decoded record, bit for bit
+  {
+    const int layers = 4, k = 8, E = 128;
+    MicroBatch rb;
+    rb.field_set = {"response", "routed_experts"};
+    unsigned x = 99;
+    auto rnd = [&]() { x = x * 1664525u + 1013904223u; return x >> 8; };
+    for (int i = 0; i < 5; ++i) {
+      const int L = 20 + static_cast<int>(rnd() % 50);
+      rb.sample_ids.push_back(static_cast<std::uint64_t>(i + 1));
+      rb.producer_versions.push_back(1);
+      rb.global_steps.push_back(1);
+      Bytes rec(static_cast<size_t>(L) * layers * k);
+      for (auto& v : rec) v = static_cast<std::uint8_t>(rnd() % E);
+      rb.payloads.push_back({enc(std::vector<int32_t>(L, 1)), rec});
+    }
+    std::vector<uint8_t> lm;
+    int64_t T = 0;
+    CHECK(staleflow::train_math::pack_routed_experts(rb, layers, k, lm, &T, &err) == SF_TM_OK);
+    void *z = nullptr, *rec_d = nullptr, *w = nullptr, *idx = nullptr;
+    cudaMalloc(&z, static_cast<size_t>(layers) * T * E * 4);
+    cudaMalloc(&rec_d, lm.size());
+    cudaMalloc(&w, lm.size() * 4);
+    cudaMalloc(&idx, lm.size() * 4);
+    cudaMemcpy(rec_d, lm.data(), lm.size(), cudaMemcpyHostToDevice);
+    CHECK(sf_tm_synth_logits(seam.handle(), z, SF_TM_F32, layers * T, E, E, 3, 2.f, nullptr, 0.f, 0.f, 0.f, nullptr) ==
+          SF_TM_OK);
+    CHECK(sf_tm_r3_gate_fwd(seam.handle(), z, SF_TM_F32, layers, T, E, k, rec_d, SF_TM_IDX_U8, 1,
+                            static_cast<float*>(w), static_cast<int32_t*>(idx), nullptr, nullptr) == SF_TM_OK);
+    std::vector<int32_t> got(lm.size());
+    cudaMemcpy(got.data(), idx, got.size() * 4, cudaMemcpyDeviceToHost);
+    bool same = true;
+    for (size_t i = 0; i < lm.size(); ++i) same &= got[i] == static_cast<int32_t>(lm[i]);
+    CHECK(same);
+    cudaFree(z);
+    cudaFree(rec_d);
+    cudaFree(w);
+    cudaFree(idx);
+  }
   std::printf(fails ? "GPU FAILED\n" : "GPU OK loss=%g active=%g\n", m1[0], m1[SF_TM_M_ACTIVE]);
 }
 #endif
