@@ -273,48 +273,76 @@ __device__ __forceinline__ void r3_load4<uint16_t>(const uint16_t* p, float (&z)
   z[0] = bf16lo(v.x); z[1] = bf16hi(v.x); z[2] = bf16lo(v.y); z[3] = bf16hi(v.y);
 }
 
-template <typename T, int NB>  // NB = E / 64 blocks of 64 experts
+// Group reductions over G lanes (G = 8 or 16).
+template <int G>
+__device__ __forceinline__ float gmaxf_g(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, G));
+  return v;
+}
+template <int G>
+__device__ __forceinline__ float gsumf_g(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+template <int G>
+__device__ __forceinline__ int gsumi_g(int v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+
+// One (layer, token) row per G-lane group, R = 32 / G rows per warp step; lane
+// gl of a group holds experts i * 4G + 4 gl + c (i < NV, c < 4). G = 8 halves
+// the per-row cost of the group reductions and of the per-row bookkeeping
+// (used when k <= 8); G = 16 covers k <= 16.
+template <typename T, int E, int G>
 __global__ void __launch_bounds__(256)
     r3_fwd_fast(const T* __restrict__ logits, int64_t L, int64_t Tn, int k, const void* __restrict__ rec,
                 int idx_dtype, int renorm, float* __restrict__ out_w, int32_t* __restrict__ out_idx,
                 uint32_t* __restrict__ mismatch) {
-  constexpr int E = NB * 64;
+  constexpr int R = 32 / G;            // rows per warp step
+  constexpr int W = 4 * G;             // experts per float4 stripe of the group
+  constexpr int NV = E / W;            // float4 per lane
+  constexpr unsigned GM = (1u << G) - 1u;
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (kG - 1);            // lane within the row group
+  const int gl = lane & (G - 1);       // lane within the row group
+  const int gi = lane / G;             // row of the step
   const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t rows = L * Tn;
-  const int64_t pairs = (rows + 1) / 2;
-  const int64_t per = (pairs + nw - 1) / nw;  // contiguous pair range per warp
+  const int64_t steps = (rows + R - 1) / R;
+  const int64_t per = (steps + nw - 1) / nw;  // contiguous step range per warp
   int64_t p0 = gw * per, p1 = p0 + per;
-  if (p1 > pairs) p1 = pairs;
+  if (p1 > steps) p1 = steps;
   int64_t cur_layer = 0, layer_end = -1;  // forces a (single) division on the first row
   uint32_t cur_cnt = 0;
-  // rows of the next pair are loaded one iteration ahead (two pairs in flight per warp)
-  float zn[NB][4];
-  int en = -1;  // next pair's recorded expert of this lane, prefetched with its logits
+  // the next step's rows (and recorded experts) are loaded one iteration ahead
+  float zn[NV][4];
+  int en = -1;
   if (p0 < p1) {
-    const int64_t r = 2 * p0 + (lane >> 4);
+    const int64_t r = R * p0 + gi;
     const int64_t rc = r < rows ? r : rows - 1;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+    for (int i = 0; i < NV; ++i) r3_load4(logits + rc * E + i * W + 4 * gl, zn[i]);
     if (gl < k) en = r3_idx(rec, idx_dtype, rc * k + gl);
   }
   for (int64_t pr = p0; pr < p1; ++pr) {
-    const int64_t row = 2 * pr + (lane >> 4);
+    const int64_t row = R * pr + gi;
     const bool valid = row < rows;
     const int64_t rowc = valid ? row : rows - 1;
-    float z[NB][4];
+    float z[NV][4];
 #pragma unroll
-    for (int i = 0; i < NB; ++i)
+    for (int i = 0; i < NV; ++i)
 #pragma unroll
       for (int c = 0; c < 4; ++c) z[i][c] = zn[i][c];
     const int my_e = en;
     if (pr + 1 < p1) {
-      const int64_t r = 2 * (pr + 1) + (lane >> 4);
+      const int64_t r = R * (pr + 1) + gi;
       const int64_t rc = r < rows ? r : rows - 1;
 #pragma unroll
-      for (int i = 0; i < NB; ++i) r3_load4(logits + rc * E + i * 64 + 4 * gl, zn[i]);
+      for (int i = 0; i < NV; ++i) r3_load4(logits + rc * E + i * W + 4 * gl, zn[i]);
       if (gl < k) en = r3_idx(rec, idx_dtype, rc * k + gl);
     }
     float zr = -INFINITY;
@@ -325,22 +353,22 @@ __global__ void __launch_bounds__(256)
     // gate weights
     float wj;
     if (renorm) {
-      const float mx = gmaxf(gl < k ? zr : -INFINITY);
+      const float mx = gmaxf_g<G>(gl < k ? zr : -INFINITY);
       const float ez = gl < k ? __expf(zr - mx) : 0.f;
-      wj = __fdividef(ez, gsumf(ez));
+      wj = __fdividef(ez, gsumf_g<G>(ez));
     } else {
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
+      for (int i = 0; i < NV; ++i)
 #pragma unroll
         for (int c = 0; c < 4; ++c) mx = fmaxf(mx, z[i][c]);
-      mx = gmaxf(mx);
+      mx = gmaxf_g<G>(mx);
       float se = 0.f;
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
+      for (int i = 0; i < NV; ++i)
 #pragma unroll
         for (int c = 0; c < 4; ++c) se += __expf(z[i][c] - mx);
-      wj = __fdividef(__expf(zr - mx), gsumf(se));
+      wj = __fdividef(__expf(zr - mx), gsumf_g<G>(se));
     }
     if (valid && gl < k) {
       out_w[row * k + gl] = wj;
@@ -349,72 +377,70 @@ __global__ void __launch_bounds__(256)
     if (mismatch) {
       // Recorded set R (k distinct valid experts) equals the trainer's top-k iff no
       // expert outside R beats in_min = min over R under (logit desc, index asc).
-      // Counting the experts above / equal to in_min decides it without knowing
-      // which lane holds which recorded expert; only an exact tie at in_min with
-      // a non-recorded expert needs the per-expert membership (rare slow path).
+      // Counting the experts >= in_min decides the common case without knowing
+      // which lane holds which recorded expert; a further expert >= in_min (a
+      // mismatch or an exact tie) goes to the per-expert slow path.
       const bool bad_e = gl < k && !(my_e >= 0 && my_e < E);
-      const unsigned key = (gl < k && !bad_e) ? ((static_cast<unsigned>(lane >> 4) << 16) | static_cast<unsigned>(my_e))
+      const unsigned key = (gl < k && !bad_e) ? ((static_cast<unsigned>(gi) << 16) | static_cast<unsigned>(my_e))
                                               : (0x80000000u | static_cast<unsigned>(lane));
       const unsigned same = __match_any_sync(0xffffffffu, key);  // every lane (no short-circuit)
       const bool dup = gl < k && __popc(same) > 1;
       const unsigned badb = __ballot_sync(0xffffffffu, bad_e || dup);
-      const bool grp_bad = ((badb >> (lane & 16)) & 0xffffu) != 0u;
+      const bool grp_bad = ((badb >> (gi * G)) & GM) != 0u;
       float in_min = (gl < k && !bad_e) ? zr : INFINITY;
 #pragma unroll
-      for (int o = kG / 2; o > 0; o >>= 1) in_min = fminf(in_min, __shfl_xor_sync(0xffffffffu, in_min, o, kG));
-      // all k recorded experts are >= in_min: any further expert >= in_min is either
-      // a mismatch or an exact tie, both settled below on the (rare) slow path
+      for (int o = G / 2; o > 0; o >>= 1) in_min = fminf(in_min, __shfl_xor_sync(0xffffffffu, in_min, o, G));
       int n_ge = 0;
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
+      for (int i = 0; i < NV; ++i)
 #pragma unroll
         for (int c = 0; c < 4; ++c) n_ge += z[i][c] >= in_min ? 1 : 0;
-      n_ge = gsumi(n_ge);
+      n_ge = gsumi_g<G>(n_ge);
       bool mm = grp_bad;
       const bool slow = !grp_bad && n_ge > k;
       if (__any_sync(0xffffffffu, slow)) {
-        // membership of my experts in the recorded set (k <= 16, unrolled)
+        // membership of my experts in the recorded set (k <= G, unrolled)
         uint32_t mine = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < G; ++j) {
           if (j < k) {
-            const int e = __shfl_sync(0xffffffffu, my_e, j, kG);
-            if (e >= 0 && e < E && ((e & 63) >> 2) == gl) mine |= 1u << ((e >> 6) * 4 + (e & 3));
+            const int e = __shfl_sync(0xffffffffu, my_e, j, G);
+            if (e >= 0 && e < E && ((e % W) >> 2) == gl) mine |= 1u << ((e / W) * 4 + (e & 3));
           }
         }
         // best non-recorded logit; on an exact tie the trainer prefers the lower index
         float out_max = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < NB; ++i)
+        for (int i = 0; i < NV; ++i)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (!((mine >> (i * 4 + c)) & 1u)) out_max = fmaxf(out_max, z[i][c]);
-        out_max = gmaxf(out_max);
+        out_max = gmaxf_g<G>(out_max);
         int in_hi = -1, out_lo = 0x7fffffff;
 #pragma unroll
-        for (int i = 0; i < NB; ++i)
+        for (int i = 0; i < NV; ++i)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int e = i * 64 + 4 * gl + c;
+            const int e = i * W + 4 * gl + c;
             const bool rin = (mine >> (i * 4 + c)) & 1u;
             if (rin && z[i][c] == in_min) in_hi = max(in_hi, e);
             if (!rin && z[i][c] == in_min) out_lo = min(out_lo, e);
           }
 #pragma unroll
-        for (int o = kG / 2; o > 0; o >>= 1) {
-          in_hi = max(in_hi, __shfl_xor_sync(0xffffffffu, in_hi, o, kG));
-          out_lo = min(out_lo, __shfl_xor_sync(0xffffffffu, out_lo, o, kG));
+        for (int o = G / 2; o > 0; o >>= 1) {
+          in_hi = max(in_hi, __shfl_xor_sync(0xffffffffu, in_hi, o, G));
+          out_lo = min(out_lo, __shfl_xor_sync(0xffffffffu, out_lo, o, G));
         }
         if (slow && (out_max > in_min || (out_max == in_min && out_lo < in_hi))) mm = true;
       }
       // per-layer counts; the layer boundary advances incrementally (no 64-bit division per row)
       const unsigned bal = __ballot_sync(0xffffffffu, valid && mm && gl == 0);
-      if (2 * pr + 1 < layer_end && 2 * pr + 1 < rows) {
-        cur_cnt += __popc(bal & 0x00010001u);  // both rows of the pair in the current layer
+      if (R * pr + (R - 1) < layer_end && R * pr + (R - 1) < rows) {
+        cur_cnt += __popc(bal);  // all rows of the step in the current layer (only gl == 0 bits)
       } else {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t rr = 2 * pr + h;
+        for (int h = 0; h < R; ++h) {
+          const int64_t rr = R * pr + h;
           if (rr >= rows) continue;
           if (rr >= layer_end) {
             if (cur_cnt && lane == 0) {
@@ -425,7 +451,7 @@ __global__ void __launch_bounds__(256)
             layer_end = (cur_layer + 1) * Tn;
             cur_cnt = 0;
           }
-          if ((bal >> (h * 16)) & 1u) ++cur_cnt;
+          if ((bal >> (h * G)) & 1u) ++cur_cnt;
         }
       }
     }
@@ -511,21 +537,22 @@ int launch_r3_fwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E
                   const void* rec_idx, int idx_dtype, int renorm, float* out_w, int32_t* out_idx,
                   uint32_t* out_mismatch, cudaStream_t s, int* launches) {
   if (E % 64 == 0 && E <= 256 && k <= 16) {
-    const int grid = r3_grid((L * T + 1) / 2);
-#define LAUNCH_FF(NB)                                                                                  \
+    const bool g8 = k <= 8 && E % 32 == 0;  // 8-lane groups: 4 rows per warp step
+    const int grid = r3_grid((L * T + (g8 ? 3 : 1)) / (g8 ? 4 : 2));
+#define LAUNCH_FF(EE, GG)                                                                              \
   if (dtype == 1)                                                                                      \
-    r3_fwd_fast<uint16_t, NB><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(logits), L, T,         \
-                                                   static_cast<int>(k), rec_idx, idx_dtype, renorm,    \
-                                                   out_w, out_idx, out_mismatch);                      \
+    r3_fwd_fast<uint16_t, EE, GG><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(logits), L, T,     \
+                                                       static_cast<int>(k), rec_idx, idx_dtype, renorm, \
+                                                       out_w, out_idx, out_mismatch);                  \
   else                                                                                                 \
-    r3_fwd_fast<float, NB><<<grid, 256, 0, s>>>(static_cast<const float*>(logits), L, T,               \
-                                                static_cast<int>(k), rec_idx, idx_dtype, renorm, out_w, \
-                                                out_idx, out_mismatch);
+    r3_fwd_fast<float, EE, GG><<<grid, 256, 0, s>>>(static_cast<const float*>(logits), L, T,           \
+                                                    static_cast<int>(k), rec_idx, idx_dtype, renorm,    \
+                                                    out_w, out_idx, out_mismatch);
     switch (E / 64) {
-      case 1: LAUNCH_FF(1) break;
-      case 2: LAUNCH_FF(2) break;
-      case 3: LAUNCH_FF(3) break;
-      default: LAUNCH_FF(4) break;
+      case 1: if (g8) { LAUNCH_FF(64, 8) } else { LAUNCH_FF(64, 16) } break;
+      case 2: if (g8) { LAUNCH_FF(128, 8) } else { LAUNCH_FF(128, 16) } break;
+      case 3: if (g8) { LAUNCH_FF(192, 8) } else { LAUNCH_FF(192, 16) } break;
+      default: if (g8) { LAUNCH_FF(256, 8) } else { LAUNCH_FF(256, 16) } break;
     }
 #undef LAUNCH_FF
     if (launches) *launches += 1;

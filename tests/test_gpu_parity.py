@@ -345,11 +345,14 @@ def test_vocab_parallel_matches_fused(tm, orc, P):
 
 
 # ---------------------------------------------------------------------------- a5 R3
-@pytest.mark.parametrize("dtype,idx_dtype,renorm", [("f32", "i32", True), ("bf16", "u8", True), ("f32", "i32", False),
-                                                    ("bf16", "i32", False)])
-def test_r3_gate(tm, orc, dtype, idx_dtype, renorm):
+@pytest.mark.parametrize("dtype,idx_dtype,renorm,E,k", [("f32", "i32", True, 128, 8), ("bf16", "u8", True, 128, 8),
+                                                        ("f32", "i32", False, 128, 8), ("bf16", "i32", False, 128, 8),
+                                                        ("f32", "u8", True, 64, 12), ("bf16", "i32", True, 256, 16),
+                                                        ("f32", "i32", True, 192, 4)])
+def test_r3_gate(tm, orc, dtype, idx_dtype, renorm, E, k):
+    """k <= 8 runs 8-lane row groups, k <= 16 16-lane groups (E % 64 == 0)."""
     rng = np.random.default_rng(41)
-    L, T, E, k = 4, 300, 128, 8
+    L, T = 4, 300
     z = (rng.normal(size=(L, T, E)) * 2).astype(np.float32)
     if dtype == "bf16":
         zb = orc.f32_to_bf16_bits(z).reshape(L, T, E)
