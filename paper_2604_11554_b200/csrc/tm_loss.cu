@@ -37,6 +37,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "tm_rowmath.cuh"
 
@@ -206,10 +207,18 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // handles the same rows, and the control warps exchange the per-row partial
 // statistics through peer-mapped global-memory mailboxes (NVLink P2P stores,
 // system-scope release/acquire) instead of DSMEM. The shard is read once.
-template <typename T, int C, bool XP = false>
+// UA (C == 1 only): rows need not start on a 16-B boundary (odd vocabularies,
+// odd row strides). Each row is then handled in "sector coordinates": the TMA
+// copies start at the row's 16-B-aligned-down address, so the row begins `mis`
+// elements into chunk 0; chunk 0 and the tail chunk are masked per element and
+// the boundary dlogits vectors are stored per element. Reads extend to whole
+// 16-B sectors inside the tensor; the very last row's tail sector is filled by
+// the producer with element loads instead, so nothing past the tensor is read.
+template <typename T, int C, bool XP = false, bool UA = false>
 __global__ void __launch_bounds__(kThreads, 1)
     loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
+  static_assert(!UA || (C == 1 && !XP), "unaligned rows run one CTA per row");
   using G = Geo<T>;
   constexpr int CE = G::CE;
   constexpr int NE = G::NE;
@@ -282,6 +291,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   unsigned long long w_a = 0, w_b = 0;  // per-role wait cycles (debug)
   const long long t_role0 = dbg ? clock64() : 0;
+  // elements between a row slice's start and its 16-B sector start (UA only)
+  auto row_mis = [&](int64_t t) -> int {
+    if constexpr (UA) {
+      return static_cast<int>((reinterpret_cast<uintptr_t>(logits + t * a.ld + slice_start) & 15u) / G::es);
+    } else {
+      (void)t;
+      return 0;
+    }
+  };
 
   if (warp == kProd) {
     // ================================================================ producer
@@ -293,14 +311,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float wcur = wn;
         if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
         if (wcur == 0.f) continue;
-        const T* row = logits + t * a.ld + slice_start;
-        for (int k = 0; k < nck; ++k) {
-          const int rem = slice_len - k * CE;
-          const uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
+        const int mis = row_mis(t);
+        const int span = slice_len + mis;
+        const int nck_r = UA ? (span + CE - 1) / CE : nck;
+        const T* row = logits + t * a.ld + slice_start - mis;
+        for (int k = 0; k < nck_r; ++k) {
+          const int rem = span - k * CE;
+          uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
+          int tail = 0;  // UA: elements of a final partial sector loaded by this lane
+          if constexpr (UA) {
+            if ((bytes & 15u) && t == a.T - 1 && k == nck_r - 1) {
+              tail = static_cast<int>((bytes & 15u) / G::es);  // never read past the tensor
+              bytes &= ~15u;
+            } else {
+              bytes = (bytes + 15u) & ~15u;  // whole sectors (inside the tensor)
+            }
+          }
           DBG_WAIT(w_a, mbar_wait(smem_u32(&empty_bar[slot]), ph ^ 1u));
-          mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes);
-          bulk_g2s(ring_base + slot * kCB, row + static_cast<int64_t>(k) * CE, bytes,
-                   smem_u32(&full_bar[slot]), pol);
+          if constexpr (UA) {
+            const T* tp = row + static_cast<int64_t>(k) * CE + bytes / G::es;
+            uint8_t* ts_ = ring + slot * kCB + bytes;
+            for (int j = 0; j < tail; ++j) reinterpret_cast<T*>(ts_)[j] = tp[j];
+          }
+          mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes);  // release: orders the tail stores
+          if (bytes)
+            bulk_g2s(ring_base + slot * kCB, row + static_cast<int64_t>(k) * CE, bytes,
+                     smem_u32(&full_bar[slot]), pol);
           if (++slot == kSlots) {
             slot = 0;
             ph ^= 1u;
@@ -351,6 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (wcur == 0.f) continue;
       (void)ycur;
+      const int mis = row_mis(t);
+      const int span = slice_len + mis;  // row extent in sector coordinates
+      const int nck_r = UA ? (span + CE - 1) / CE : nck;
       float m2 = 0.f;
       // two float2 partial sums = 4 independent chains, updated with FADD2/FFMA2
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -386,14 +425,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float x[NE];
         unpack(logits, v0, v1, x);
-        const int rem = slice_len - k * CE;
+        const int rem = span - k * CE;             // valid elements end here (chunk coordinates)
+        const int lo = (UA && k == 0) ? mis : 0;   // ... and start here
         if (first) {
           // Later elements may exceed this base (arguments > 0 are fine); only a
           // jump of > 126 in log2 units overflows, which the row-end repair handles.
           float xm = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (!partial || elem_off<T>(ftid, j) < rem) xm = fmaxf(xm, x[j]);
+          for (int j = 0; j < NE; ++j) {
+            const int pj = elem_off<T>(ftid, j);
+            if (!partial || (pj >= lo && pj < rem)) xm = fmaxf(xm, x[j]);
+          }
           m2 = xm * c;
           if (!(m2 > -INFINITY)) m2 = 0.f;  // nothing finite: any finite base works
         }
@@ -408,10 +450,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             s2[p & 1] = __fadd2_rn(s2[p & 1], e);
             w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
           }
+        } else if (UA) {
+          // unaligned row, front or tail chunk: packed math on vectors wholly
+          // inside the row, element masks only on the (at most two) boundary
+          // vectors of the chunk
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p0 = v * G::HALF + EV * ftid;
+            if (p0 >= lo && p0 + EV <= rem) {
+#pragma unroll
+              for (int q = 0; q < EV / 2; ++q) {
+                const int p = v * (EV / 2) + q;
+                const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
+                const float2 e = make_float2(ex2(av.x), ex2(av.y));
+                s2[p & 1] = __fadd2_rn(s2[p & 1], e);
+                w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
+              }
+            } else if (p0 + EV > lo && p0 < rem) {
+#pragma unroll
+              for (int j = 0; j < EV; ++j) {
+                const int pj = p0 + j;
+                if (pj >= lo && pj < rem && x[v * EV + j] != -INFINITY) {
+                  const float av = fmaf(x[v * EV + j], c, -m2);
+                  const float e = ex2(av);
+                  s2[0].x += e;
+                  w2[0].x = fmaf(e, av, w2[0].x);
+                }
+              }
+            }
+          }
         } else {
-          // Partial chunk. Slice lengths are multiples of the 16-B vector (the
-          // ring path requires it), so each of this thread's two vectors lies
-          // wholly inside or outside the slice: the packed path, per vector.
+          // Partial chunk. Aligned slice lengths are multiples of the 16-B
+          // vector, so each of this thread's two vectors lies wholly inside or
+          // outside the slice: the packed path, per vector.
           // A -inf logit makes w NaN here as on full chunks -> row-end repair.
           const bool ok0 = EV * ftid < rem, ok1 = G::HALF + EV * ftid < rem;
           const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
@@ -435,7 +507,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
       };
-      if (nck == 0) {
+      if constexpr (UA) {
+        // peeled like the aligned schedule: only the front and tail chunks are masked
+        const int nfull_r = span / CE;
+        if (nck_r > 0) {
+          if (mis > 0 || span < CE) {
+            chunk(0, true, true);
+          } else {
+            chunk(0, true, false);
+          }
+          for (int k = 1; k < nfull_r; ++k) chunk(k, false, false);
+          if (nck_r > nfull_r && nck_r > 1) chunk(nck_r - 1, false, true);
+        }
+      } else if (nck == 0) {
         // empty slice (a cluster wider than the vocab): contributes nothing
       } else if (nfull == 0) {
         chunk(0, true, true);
@@ -452,29 +536,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (__any_sync(0xffffffffu, bad)) {
         float mx = -INFINITY;
         uint32_t q = ts0;
-        for (int k = 0; k < nck; ++k) {
+        for (int k = 0; k < nck_r; ++k) {
           uint4 v0r, v1r;
           load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
-          const int rem = slice_len - k * CE;
+          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (elem_off<T>(ftid, j) < rem) mx = fmaxf(mx, x[j]);
+          for (int j = 0; j < NE; ++j) {
+            const int pj = elem_off<T>(ftid, j);
+            if (pj >= lo && pj < rem) mx = fmaxf(mx, x[j]);
+          }
           if (++q == kStore) q = 0;
         }
         const float mb2 = (mx == -INFINITY) ? -INFINITY : mx * c;
         float sr = 0.f, wr = 0.f;
         q = ts0;
-        for (int k = 0; k < nck; ++k) {
+        for (int k = 0; k < nck_r; ++k) {
           uint4 v0r, v1r;
           load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
-          const int rem = slice_len - k * CE;
+          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
-            if (elem_off<T>(ftid, j) < rem && x[j] != -INFINITY) {
+            const int pj = elem_off<T>(ftid, j);
+            if (pj >= lo && pj < rem && x[j] != -INFINITY) {
               const float av = fmaf(x[j], c, -mb2);
               const float e = ex2(av);
               sr += e;
@@ -781,12 +868,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
       if (w == 0.f) {
         if (!a.masked_skip) {
-          uint8_t* drow = reinterpret_cast<uint8_t*>(static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start);
-          const int nb = slice_len * G::es;
-          for (int off = btid * 16; off < nb; off += kFT * 16) stg128_cs(drow + off, make_uint4(0, 0, 0, 0));
+          T* drow0 = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
+          if constexpr (UA) {
+            // element stores up to the first 16-B sector, vectors, element tail
+            const int head = static_cast<int>(((16u - (reinterpret_cast<uintptr_t>(drow0) & 15u)) & 15u) / G::es);
+            const int h = head < slice_len ? head : slice_len;
+            if (btid < h) st1(drow0 + btid, 0.f);
+            uint8_t* mid = reinterpret_cast<uint8_t*>(drow0 + h);
+            const int nv = (slice_len - h) / EV;
+            for (int i = btid; i < nv; i += kFT) stg128_cs(mid + 16 * i, make_uint4(0, 0, 0, 0));
+            const int tl = h + nv * EV;
+            if (btid < slice_len - tl) st1(drow0 + tl + btid, 0.f);
+          } else {
+            uint8_t* drow = reinterpret_cast<uint8_t*>(drow0);
+            const int nb = slice_len * G::es;
+            for (int off = btid * 16; off < nb; off += kFT * 16) stg128_cs(drow + off, make_uint4(0, 0, 0, 0));
+          }
         }
         continue;
       }
+      const int mis = row_mis(t);
+      const int span = slice_len + mis;  // row extent in sector coordinates
+      const int nck_r = UA ? (span + CE - 1) / CE : nck;
       const uint32_t rs = nrow % kRD;
       const uint32_t rpar = (nrow / kRD) & 1u;
       DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
@@ -795,15 +898,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool neg = rsc.sgn != 0u;
       int ck = -1, jt = 0;
       if (rsc.yl >= 0) {
-        const int r = rsc.yl % CE;
+        const int yp = rsc.yl + mis;  // sector coordinates
+        const int r = yp % CE;
         const int v = r >= G::HALF ? 1 : 0;
         const int rr = r - v * G::HALF;
         if (rr / EV == btid) {
-          ck = rsc.yl / CE;
+          ck = yp / CE;
           jt = v * EV + rr % EV;
         }
       }
-      T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
+      // dlogits rows share the logits rows' sector phase (checked at dispatch)
+      T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start - mis;
       const uint32_t sgn = neg ? 0x80008000u : 0u;
       const float gts = neg ? -gt : gt;  // target term before the sign flip
       // One chunk of dlogits. MODE (row-uniform): 0 = bf16 with |c0| folded
@@ -834,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
         T* dst = drow + k * CE;
-        const int rem = slice_len - k * CE;
+        const int rem = span - k * CE;
         if (!partial && (dbg_mode & 2)) {  // debug: store the words back (pipeline ceiling)
           if (!(dbg_mode & 4)) {
             stg128_cs(dst + EV * btid, w0);
@@ -860,6 +965,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < NE; ++j)
               if (j == jt) gr[j] += gts;
+          }
+          if (UA && partial) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j) gr[j] = neg ? -gr[j] : gr[j];
+            goto general_store;
           }
           uint4 p0, p1;
           p0.x = pack_bf16x2(gr[0], gr[1]) ^ sgn;
@@ -911,9 +1021,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (j == jt) gr[j] += gt;
           }
         }
+      general_store:
         if (!partial) {
           store_vec(dst + EV * btid, gr);
           store_vec(dst + G::HALF + EV * btid, gr + EV);
+        } else if (UA) {
+          // front/tail chunk of an unaligned row: whole vectors where they are
+          // entirely inside the row, element stores on the boundary vectors
+          const int lo = (k == 0) ? mis : 0;
+          bool any = false;
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p0 = v * G::HALF + EV * btid;
+            if (p0 >= lo && p0 + EV <= rem) {
+              store_vec(dst + p0, gr + v * EV);
+              any = true;
+            } else {
+#pragma unroll
+              for (int j = 0; j < EV; ++j)
+                if (p0 + j >= lo && p0 + j < rem) {
+                  st1(dst + p0 + j, gr[v * EV + j]);
+                  any = true;
+                }
+            }
+          }
+          if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]));
         } else {
           const bool s0 = EV * btid < rem;
           if (s0) store_vec(dst + EV * btid, gr);
@@ -923,7 +1055,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (late) mbar_arrive(rel);
       };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
-      if (mode == 0) {
+      if constexpr (UA) {
+        const int nfull_r = span / CE;
+        const bool front = mis > 0 || span < CE;
+        auto sched = [&](auto md) {
+          constexpr int M = decltype(md)::value;
+          if (nck_r == 0) return;
+          if (front) {
+            bchunk(0, true, M);
+          } else {
+            bchunk(0, false, M);
+          }
+          for (int k = 1; k < nfull_r; ++k) bchunk(k, false, M);
+          if (nck_r > nfull_r && nck_r > 1) bchunk(nck_r - 1, true, M);
+        };
+        if (mode == 0) {
+          sched(std::integral_constant<int, 0>{});
+        } else if (mode == 1) {
+          sched(std::integral_constant<int, 1>{});
+        } else {
+          sched(std::integral_constant<int, 2>{});
+        }
+      } else if (mode == 0) {
         for (int k = 0; k < nfull; ++k) bchunk(k, false, 0);
         if (nck > nfull) bchunk(nfull, true, 0);
       } else if (mode == 1) {
@@ -935,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // the row's stores consumed every lane's scalars (a row with no chunk
       // here consumes them through a dependent dummy smem store): free the slot
-      if (nck == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.yl);
+      if (nck_r == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.yl);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;
@@ -959,9 +1112,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
-template <typename T, int C, bool XP = false>
+template <typename T, int C, bool XP = false, bool UA = false>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  auto kern = loss_tmem_kernel<T, C, XP>;
+  auto kern = loss_tmem_kernel<T, C, XP, UA>;
   static int max_active = -1;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1050,6 +1203,13 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
     slice = (slice + G::EV - 1) / G::EV * G::EV;
     return (slice + G::CE - 1) / G::CE;
   };
+  // Rows not on 16-B boundaries (odd vocabulary or stride): one CTA per row in
+  // sector coordinates; the row may straddle one extra chunk.
+  const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
+  if (ua) {
+    if ((a.V + G::EV - 1 + G::CE - 1) / G::CE > kMaxChunks) return -2;
+    return launch_c<T, 1, false, true>(a, a.V, s, info);
+  }
   static const int forced = [] {  // tuning knob: SFTM_LOSS_C=1|2|3|4|8
     const char* v = getenv("SFTM_LOSS_C");
     return v ? atoi(v) : 0;

@@ -549,8 +549,14 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
     aligned_out = (reinterpret_cast<uintptr_t>(a.dlogits) % 16 == 0) && ((a.ld_d * es) % 16 == 0);
   const bool ring_ok = !g_force_generic && aligned_in && aligned_out;
   const int CB = kChunkElems * es;
+  // The fused loss also takes rows off 16-B boundaries (odd vocabularies or
+  // strides) as long as dlogits rows sit at the same sector phase as the logits
+  // rows (same base alignment mod 16, stride difference a multiple of 16 B).
+  const uintptr_t lb = reinterpret_cast<uintptr_t>(a.logits), db = reinterpret_cast<uintptr_t>(a.dlogits);
+  const bool ua_ok = !g_force_generic && mode == kModeFwdBwd && lb % es == 0 && db % es == 0 &&
+                     (lb % 16) == (db % 16) && (((a.ld_d - a.ld) * es) % 16 == 0);
 
-  if (ring_ok) {
+  if (ring_ok || ua_ok) {
     if (mode == kModeFwdBwd) {
       // default: role-split schedule (tm_loss.cu); SFTM_LOSS_VARIANT=3 selects the
       // per-warp software-pipelined schedule (tm_loss3.cu) for A/B comparisons
@@ -558,7 +564,7 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
         const char* v = getenv("SFTM_LOSS_VARIANT");
         return (v && v[0] == '3') ? 3 : 2;
       }();
-      const int e = variant == 2 ? launch_loss_tmem(a, s, info) : launch_loss_v3(a, s, info);
+      const int e = (variant == 2 || !ring_ok) ? launch_loss_tmem(a, s, info) : launch_loss_v3(a, s, info);
       if (e != -2) return e;  // -2: slice too wide for TMEM residency -> generic
     } else {
       const int nslots = kStreamRingBytes / CB;

@@ -211,7 +211,11 @@ LOSS_CASES = [
     ("seq_mean_bf16", "bf16", 32000, [25, 5, 25], {}, {"norm_mode": 1}),
     ("f32_wide_c4", "f32", 151936, [6, 4], {}, {}),
     ("bf16_c8_262k", "bf16", 262144, [5], {}, {}),
-    ("bf16_odd_vocab_generic", "bf16", 50257, [10, 7], {}, {}),
+    ("bf16_odd_vocab", "bf16", 50257, [10, 7, 40, 3], {}, {}),
+    ("f32_odd_vocab_kl_ent", "f32", 32001, [20, 13], {"kl_beta": 0.05, "entropy_coef": 0.01}, {}),
+    ("bf16_odd_vocab_ent_inplace", "bf16", 50257, [9, 30], {"entropy_coef": 0.02}, {"in_place": True}),
+    ("bf16_odd_vocab_skip", "bf16", 20011, [25, 25], {}, {"masked_skip": True}),
+    ("bf16_odd_tiny", "bf16", 13, [9, 9], {}, {}),
     ("bf16_tiny_vocab", "bf16", 16, [9, 9], {"kl_beta": 0.1}, {}),
 ]
 
@@ -221,6 +225,40 @@ def test_pg_loss_fwd_bwd(tm, orc, case):
     _, dtype, V, lens, pkw, kw = case
     prob = orc.synth_problem(abs(hash(case[0])) % 1000, lens, V, dtype, prompt_max=8)
     check_loss_case(tm, orc, prob, pkw, **kw)
+
+
+def test_pg_loss_unaligned_rows_use_fused_kernel(tm, orc):
+    """Odd vocabularies and odd row strides run the fused single-pass kernel
+    (rows handled in 16-B sector coordinates), not the two-pass fallback; a
+    dlogits buffer at a different sector phase falls back and still agrees."""
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(9, [33, 20, 51], 4099, "bf16", prompt_max=8)
+    T, V = len(prob["targets"]), 4099
+    base = torch.zeros(T, V + 5, dtype=torch.bfloat16, device="cuda")
+    view = base[:, 3:3 + V]  # odd stride (V + 5) and a 6-byte row offset
+    view.copy_(to_dev_logits(prob))
+    cu, sid, mask, adv, adv_tok, w_tok = gpu_pipeline(tm, prob, 0)
+    params = _lib.default_loss_params()
+    dl = torch.zeros_like(base)[:, 3:3 + V]
+    met, dl, logp, ent = tm.pg_loss_fwd_bwd(view, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]),
+                                            adv_tok, w_tok, params, dlogits=dl, want_logp=True)
+    torch.cuda.synchronize()
+    assert tm.handle().last_launch()["kernel"] == "loss_tmem_kernel"
+    om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"],
+                                                 adv_tok.cpu().numpy(), w_tok.cpu().numpy(), orc.params())
+    act = w_tok.cpu().numpy() != 0
+    assert_close(logp.cpu().numpy()[act], olp[act], what="logp")
+    near = near_clip_rows(olp, prob["old"], adv_tok.cpu().numpy(), 0.2, 0.28)
+    assert_grad_close(grad_to_np(dl), odl, np.abs(og), "bf16", rows_ok=~near)
+    # dlogits at another sector phase: generic fallback, same answer
+    dl2 = torch.zeros(T, V + 1, dtype=torch.bfloat16, device="cuda")[:, :V]
+    met2, dl2, _, _ = tm.pg_loss_fwd_bwd(view, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]),
+                                         adv_tok, w_tok, params, dlogits=dl2)
+    torch.cuda.synchronize()
+    assert tm.handle().last_launch()["kernel"] == "rows_generic_kernel"
+    assert_grad_close(grad_to_np(dl2), odl, np.abs(og), "bf16", rows_ok=~near)
+    assert np.allclose(met2.cpu().numpy()[:6], met.cpu().numpy()[:6], rtol=1e-5, atol=1e-7)
 
 
 def test_pg_loss_deterministic(tm, orc):
