@@ -118,7 +118,7 @@ uint64_t sf_tm_launch_count(sf_tm_t h);
 /* Which row kernel the last row-kernel call on this handle launched:
  * *kernel 0 = streaming TMA ring, 1 = generic two-pass, 2 = fused TMEM/smem
  * row-store loss kernel, 3 = its per-warp pipelined variant, 4 = the fused
- * vocab-parallel (peer-mailbox) kernel; *cluster = CTAs
+ * vocab-parallel (peer-mailbox) kernel, 5 = the forward-only streaming kernel; *cluster = CTAs
  * per row; *grid = CTAs launched. Any pointer may be NULL. */
 int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* grid);
 

@@ -87,6 +87,8 @@ int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, La
 // Fused vocab-parallel loss (one CTA per SM, peer-mailbox exchange); -2 if the
 // shard is not eligible (then the caller reports a config error).
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info);
+// Forward-only streaming pass (kModeFwd / kModeVpStats) on 16-B aligned rows (tm_fwd.cu).
+int launch_fwd_stream(const RowArgs& a, int mode, cudaStream_t s, LaunchInfo* info);
 
 // Forces the generic (non-TMA) kernel; used by tests to cover both paths.
 void set_force_generic(bool on);

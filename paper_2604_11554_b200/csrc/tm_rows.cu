@@ -567,6 +567,16 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
       const int e = (variant == 2 || !ring_ok) ? launch_loss_tmem(a, s, info) : launch_loss_v3(a, s, info);
       if (e != -2) return e;  // -2: slice too wide for TMEM residency -> generic
     } else {
+      // forward-only modes: the 24-warp streaming kernel (tm_fwd.cu);
+      // SFTM_FWD_RING=1 selects the older 16-warp ring kernel for A/B runs
+      static const bool old_ring = [] {
+        const char* v = getenv("SFTM_FWD_RING");
+        return v && v[0] == '1';
+      }();
+      if (ring_ok && !old_ring && (mode == kModeFwd || mode == kModeVpStats)) {
+        const int e = launch_fwd_stream(a, mode, s, info);
+        if (e != -2) return e;
+      }
       const int nslots = kStreamRingBytes / CB;
       const int ring_bytes = nslots * CB;
       switch (mode) {

@@ -62,7 +62,7 @@ class Handle:
         self.check(_lib.lib().sf_tm_last_launch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(g)),
                    "sf_tm_last_launch")
         names = {0: "rows_ring_kernel", 1: "rows_generic_kernel", 2: "loss_tmem_kernel", 3: "loss_v3_kernel",
-                 4: "loss_tmem_kernel[peer-exchange]"}
+                 4: "loss_tmem_kernel[peer-exchange]", 5: "fwd_stream_kernel"}
         return {"kernel": names.get(k.value, str(k.value)), "cluster": c.value, "grid": g.value}
 
     def close(self):
