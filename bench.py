@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     ap.add_argument("--generic", action="store_true", help="force the generic two-pass kernel (comparison)")
+    ap.add_argument("--fwd-only", action="store_true",
+                    help="a1 forward only (ActorFwd / RefLogP logp+entropy) on the config-2 micro-batch shape")
     ap.add_argument("--vp-two-pass", action="store_true",
                     help="config 5: stats kernel + NCCL all_gather + backward kernel instead of the fused "
                          "single-pass kernel with the in-kernel peer exchange (comparison)")
@@ -236,10 +238,12 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    if args.config != 2:
+    if args.config != 2 or args.fwd_only:
         import bench_extra
 
-        if args.config in (1, 4):
+        if args.fwd_only:
+            bench_extra.run_fwd_only(args, world, rank, dev, dist)
+        elif args.config in (1, 4):
             bench_extra.run_loss_config(args, args.config, world, rank, dev, dist)
         elif args.config == 3:
             bench_extra.run_r3(args, world, rank, dev, dist)

@@ -169,6 +169,57 @@ def run_loss_config(args, cfg, world, rank, dev, dist):
                                                                     **h.last_launch())}, clocks, int(launches))
 
 
+def run_fwd_only(args, world, rank, dev, dist):
+    """a1 forward only: per-token logp + entropy + lse of every token (the
+    ActorFwd / RefLogP stage payloads), config-2 shape: 16 micro-batches of
+    32 x 4096 tokens, Qwen3 vocab bf16. 2V bytes per token."""
+    import torch
+
+    from paper_2604_11554_b200 import train_math as tm
+
+    V, M, T_mb = args.vocab, args.micro_batches, args.seqs_per_mb * args.seq_len
+    logits = torch.empty(T_mb, V, dtype=torch.bfloat16, device=dev)
+    tm.synth_logits(logits, seed=11 + rank, sigma=2.0)
+    g = torch.Generator(device=dev).manual_seed(3 + rank)
+    targets = torch.randint(0, V, (M * T_mb,), device=dev, dtype=torch.int32, generator=g)
+    out_lp = torch.empty(M * T_mb, device=dev)
+    out_h = torch.empty(M * T_mb, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    h = tm.handle(dev.index)
+
+    def step(rec):
+        ev = []
+        for m in range(M):
+            sl = slice(m * T_mb, (m + 1) * T_mb)
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if rec else None
+            if rec:
+                e[0].record(stream)
+            lp, ent, _ = tm.logprob_fwd(logits, targets[sl])
+            out_lp[sl].copy_(lp)
+            out_h[sl].copy_(ent)
+            if rec:
+                e[1].record(stream)
+                ev.append(e)
+        return ev
+
+    l0 = h.launch_count()
+    ms_step, kms, clocks = _timed(step, args.steps, args.warmup, dev, world, dist, stream)
+    launches = h.launch_count() - l0
+    pk, src = _peak()
+    by = T_mb * V * 2 + T_mb * 16
+    ach = by / (kms / 1e3) / 1e9
+    _line(args, world, "tokens/s fused logprob+entropy forward (ActorFwd/RefLogP, Qwen3-4B vocab)",
+          world * M * T_mb / (ms_step / 1e3), ms_step, "bf16",
+          {"workload": f"a1 forward only: {M} x ({args.seqs_per_mb} x {args.seq_len} tok), vocab {V} bf16",
+           "tokens_per_step": world * M * T_mb, "vocab": V, "parallelism": f"dp{world}",
+           "l2": "inputs >> L2 (no flush)"},
+          {"bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
+           "peak_source": src + " (copy = read+write; a read-only stream can exceed it)",
+           "algorithmic_bytes_per_launch": by, "avg_launch_ms": kms,
+           "kernel": "{kernel}<bf16,C={cluster}> grid {grid}".format(**h.last_launch()),
+           "bytes_model": "2V B per token read + 16 B/token scalars"}, clocks, int(launches))
+
+
 def run_r3(args, world, rank, dev, dist):
     """Config 3: R3 replay gate fwd+bwd, 48 layers x 128 experts top-8, fp32 router logits."""
     import torch

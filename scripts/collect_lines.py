@@ -21,10 +21,12 @@ def last_line(path):
 def main():
     what = sys.argv[1]
     if what == "configs":
-        for c in (1, 3, 4, 5):
-            d = last_line(os.path.join(OUT, f"cfg{c}.log"))
+        for c in (1, 3, 4, 5, "_fwd"):
+            p = os.path.join(OUT, f"cfg{c}.log")
+            d = last_line(p) if os.path.exists(p) else None
             if d:
-                json.dump(d, open(os.path.join(PROF, f"r1_bench_config{c}.json"), "w"), indent=1)
+                name = "r1_bench_fwd_only.json" if c == "_fwd" else f"r1_bench_config{c}.json"
+                json.dump(d, open(os.path.join(PROF, name), "w"), indent=1)
                 print(c, d["value"], d.get("roofline", {}).get("frac"))
     elif what == "scaling":
         path = os.path.join(PROF, "r1_scaling.json")
