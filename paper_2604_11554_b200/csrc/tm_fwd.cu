@@ -7,7 +7,8 @@
 //
 // sm_100a structure (one CTA per SM, persistent, rows grid-strided):
 //   warp 24      TMA producer: cp.async.bulk 12 KB chunks of each row into two
-//                8-slot smem rings (192 KB), chunk k of a row into ring k % 2,
+//                8-slot smem rings (192 KB), chunk k of row r into ring (k + r) % 2
+//                (rows alternate which group starts, balancing odd chunk counts),
 //                L2 evict-first, running ahead across rows.
 //   warps 0..23  two groups of 12 forward warps; group g consumes ring g in
 //                order (a plain single-consumer ring per group). Each thread folds its 16 elements per chunk into an
@@ -25,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "tm_rowmath.cuh"
 
@@ -70,7 +72,11 @@ __device__ __forceinline__ int elem_off(int tid, int j) {
   return (j < G::EV) ? (G::EV * tid + j) : (G::HALF + G::EV * tid + (j - G::EV));
 }
 
-template <typename T, int MODE>
+// UA: rows off 16-B boundaries (odd vocabulary / stride), handled in sector
+// coordinates exactly as the fused kernel does (tm_loss.cu): a row starts
+// `mis` elements into its first sector; front/tail chunks are masked; the last
+// row's final partial sector is loaded by the producer element-wise.
+template <typename T, int MODE, bool UA>
 __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a) {
   using G = Geo<T>;
   constexpr int CE = G::CE;
@@ -91,6 +97,14 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
   const int nck = (V + CE - 1) / CE;
   const uint32_t ring_base = smem_u32(ring);
   const T* logits = static_cast<const T*>(a.logits);
+  auto row_mis = [&](int64_t t) -> int {
+    if constexpr (UA) {
+      return static_cast<int>((reinterpret_cast<uintptr_t>(logits + t * a.ld) & 15u) / G::es);
+    } else {
+      (void)t;
+      return 0;
+    }
+  };
 
   if (tid == 0) {
     for (int g = 0; g < 2; ++g)
@@ -111,16 +125,35 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       uint32_t slot[2] = {0, 0}, ph[2] = {0, 0};
-      for (int64_t t = cid; t < a.T; t += ncl) {
-        const T* row = logits + t * a.ld;
-        for (int k = 0; k < nck; ++k) {
-          const int g = k & 1;
-          const int rem = V - k * CE;
-          const uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
+      uint32_t nrow = 0;
+      for (int64_t t = cid; t < a.T; t += ncl, ++nrow) {
+        const int mis = row_mis(t);
+        const int span = V + mis;
+        const int nck_r = UA ? (span + CE - 1) / CE : nck;
+        const T* row = logits + t * a.ld - mis;
+        for (int k = 0; k < nck_r; ++k) {
+          const int g = (k + static_cast<int>(nrow)) & 1;  // alternate the first group per row
+          const int rem = span - k * CE;
+          uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
+          int tail = 0;
+          if constexpr (UA) {
+            if ((bytes & 15u) && t == a.T - 1 && k == nck_r - 1) {
+              tail = static_cast<int>((bytes & 15u) / G::es);  // never read past the tensor
+              bytes &= ~15u;
+            } else {
+              bytes = (bytes + 15u) & ~15u;
+            }
+          }
           mbar_wait(smem_u32(&empty_bar[g][slot[g]]), ph[g] ^ 1u);
+          if constexpr (UA) {
+            const T* tp = row + static_cast<int64_t>(k) * CE + bytes / G::es;
+            T* td = reinterpret_cast<T*>(ring + (g * kSlots + slot[g]) * kCB + bytes);
+            for (int j = 0; j < tail; ++j) td[j] = tp[j];
+          }
           mbar_arrive_expect_tx(smem_u32(&full_bar[g][slot[g]]), bytes);
-          bulk_g2s(ring_base + (g * kSlots + slot[g]) * kCB, row + static_cast<int64_t>(k) * CE, bytes,
-                   smem_u32(&full_bar[g][slot[g]]), pol);
+          if (bytes)
+            bulk_g2s(ring_base + (g * kSlots + slot[g]) * kCB, row + static_cast<int64_t>(k) * CE, bytes,
+                     smem_u32(&full_bar[g][slot[g]]), pol);
           if (++slot[g] == kSlots) {
             slot[g] = 0;
             ph[g] ^= 1u;
@@ -139,25 +172,32 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
     const uint32_t sink_a = smem_u32(&sink_sh[warp]);
     uint32_t slot = 0, ph = 0, nrow = 0;
     for (int64_t t = cid; t < a.T; t += ncl) {
+      const int mis = row_mis(t);
+      const int span = V + mis;
+      const int nck_r = UA ? (span + CE - 1) / CE : nck;
       float m2 = 0.f;
       bool have = false;
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      for (int k = grp; k < nck; k += 2) {
+      const int k0 = (grp + static_cast<int>(nrow)) & 1;  // rows alternate which group starts
+      for (int k = k0; k < nck_r; k += 2) {
         mbar_wait(full0 + 8u * slot, ph);
         const uint32_t sa = ring_t + slot * kCB;
         const uint4 v0 = lds128(sa);
         const uint4 v1 = lds128(sa + kCB / 2);
         float x[NE];
         unpack(logits, v0, v1, x);
-        const int rem = V - k * CE;
-        const bool partial = rem < CE;
+        const int rem = span - k * CE;
+        const int lo = (UA && k == 0) ? mis : 0;
+        const bool partial = rem < CE || lo > 0;
         if (!have) {
           // exponent base: this thread's max of its first chunk in the row
           float xm = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (!partial || elem_off<T>(gtid, j) < rem) xm = fmaxf(xm, x[j]);
+          for (int j = 0; j < NE; ++j) {
+            const int pj = elem_off<T>(gtid, j);
+            if (!partial || (pj >= lo && pj < rem)) xm = fmaxf(xm, x[j]);
+          }
           m2 = xm * c;
           if (!(m2 > -INFINITY)) m2 = 0.f;
           have = true;
@@ -170,6 +210,34 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
             const float2 e = make_float2(ex2(av.x), ex2(av.y));
             s2[p & 1] = __fadd2_rn(s2[p & 1], e);
             w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
+          }
+        } else if (UA) {
+          // packed math on vectors wholly inside the row, element masks on the
+          // (at most two) boundary vectors
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p0 = v * G::HALF + EV * gtid;
+            if (p0 >= lo && p0 + EV <= rem) {
+#pragma unroll
+              for (int q = 0; q < EV / 2; ++q) {
+                const int p = v * (EV / 2) + q;
+                const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
+                const float2 e = make_float2(ex2(av.x), ex2(av.y));
+                s2[p & 1] = __fadd2_rn(s2[p & 1], e);
+                w2[p & 1] = __ffma2_rn(e, av, w2[p & 1]);
+              }
+            } else if (p0 + EV > lo && p0 < rem) {
+#pragma unroll
+              for (int j = 0; j < EV; ++j) {
+                const int pj = p0 + j;
+                if (pj >= lo && pj < rem && x[v * EV + j] != -INFINITY) {
+                  const float av = fmaf(x[v * EV + j], c, -m2);
+                  const float e = ex2(av);
+                  s2[0].x += e;
+                  w2[0].x = fmaf(e, av, w2[0].x);
+                }
+              }
+            }
           }
         } else {
           // vector-granular tail (slice lengths are multiples of the 16-B vector)
@@ -199,24 +267,24 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
       // recompute this thread's partials exactly from global memory.
       const bool bad = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f);
       if (__any_sync(0xffffffffu, bad)) {
-        const T* row = logits + t * a.ld;
+        const T* row = logits + t * a.ld - mis;  // sector coordinates
         float mx = -INFINITY;
-        for (int k = grp; k < nck; k += 2) {
-          const int rem = V - k * CE;
+        for (int k = k0; k < nck_r; k += 2) {
+          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
             const int o = elem_off<T>(gtid, j);
-            if (o < rem) mx = fmaxf(mx, ldg_elem(row, static_cast<int64_t>(k) * CE + o));
+            if (o >= lo && o < rem) mx = fmaxf(mx, ldg_elem(row, static_cast<int64_t>(k) * CE + o));
           }
         }
         const float mb2 = (mx == -INFINITY) ? -INFINITY : mx * c;
         float sr = 0.f, wr = 0.f;
-        for (int k = grp; k < nck; k += 2) {
-          const int rem = V - k * CE;
+        for (int k = k0; k < nck_r; k += 2) {
+          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
             const int o = elem_off<T>(gtid, j);
-            if (o < rem) {
+            if (o >= lo && o < rem) {
               const float xv = ldg_elem(row, static_cast<int64_t>(k) * CE + o);
               if (xv != -INFINITY) {
                 const float av = fmaf(xv, c, -mb2);
@@ -273,9 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_stream_kernel(const RowArgs a
 
 std::mutex g_mu;
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool UA>
 int launch(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
-  auto kern = fwd_stream_kernel<T, MODE>;
+  auto kern = fwd_stream_kernel<T, MODE, UA>;
   static int sms = -1;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -302,14 +370,21 @@ int launch(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
 
 }  // namespace fwd
 
-// Forward-only streaming pass for kModeFwd / kModeVpStats on 16-B aligned rows.
+// Forward-only streaming pass for kModeFwd / kModeVpStats; rows off 16-B
+// boundaries run in sector coordinates (UA).
 int launch_fwd_stream(const RowArgs& a, int mode, cudaStream_t s, LaunchInfo* info) {
   if (a.V > (int64_t(1) << 30)) return -2;
-  if (a.dtype == 1) {
-    return mode == kModeVpStats ? fwd::launch<uint16_t, kModeVpStats>(a, s, info)
-                                : fwd::launch<uint16_t, kModeFwd>(a, s, info);
-  }
-  return mode == kModeVpStats ? fwd::launch<float, kModeVpStats>(a, s, info) : fwd::launch<float, kModeFwd>(a, s, info);
+  const int es = a.dtype == 1 ? 2 : 4;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(a.logits);
+  if (base % es) return -2;
+  const bool ua = (base % 16) || ((a.ld * es) % 16) || ((a.V * es) % 16);
+  auto go = [&](auto tag, auto ua_c) -> int {
+    using T = decltype(tag);
+    constexpr bool U = decltype(ua_c)::value;
+    return mode == kModeVpStats ? fwd::launch<T, kModeVpStats, U>(a, s, info) : fwd::launch<T, kModeFwd, U>(a, s, info);
+  };
+  if (a.dtype == 1) return ua ? go(uint16_t{}, std::true_type{}) : go(uint16_t{}, std::false_type{});
+  return ua ? go(float{}, std::true_type{}) : go(float{}, std::false_type{});
 }
 
 }  // namespace sftm

@@ -556,7 +556,9 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
   const bool ua_ok = !g_force_generic && mode == kModeFwdBwd && lb % es == 0 && db % es == 0 &&
                      (lb % 16) == (db % 16) && (((a.ld_d - a.ld) * es) % 16 == 0);
 
-  if (ring_ok || ua_ok) {
+  // forward-only modes: any element-aligned rows (unaligned ones in sector coordinates)
+  const bool fwd_ok = !g_force_generic && (mode == kModeFwd || mode == kModeVpStats) && lb % es == 0;
+  if (ring_ok || ua_ok || fwd_ok) {
     if (mode == kModeFwdBwd) {
       // default: role-split schedule (tm_loss.cu); SFTM_LOSS_VARIANT=3 selects the
       // per-warp software-pipelined schedule (tm_loss3.cu) for A/B comparisons
@@ -573,18 +575,20 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
         const char* v = getenv("SFTM_FWD_RING");
         return v && v[0] == '1';
       }();
-      if (ring_ok && !old_ring && (mode == kModeFwd || mode == kModeVpStats)) {
+      if (!old_ring && (mode == kModeFwd || mode == kModeVpStats)) {
         const int e = launch_fwd_stream(a, mode, s, info);
         if (e != -2) return e;
       }
       const int nslots = kStreamRingBytes / CB;
       const int ring_bytes = nslots * CB;
-      switch (mode) {
-        case kModeFwd: return launch_ring<T, 1, kModeFwd, 2>(a, a.V, nslots, ring_bytes, s, info);
-        case kModeVpStats:
-          return launch_ring<T, 1, kModeVpStats, 2>(a, a.V, nslots, ring_bytes, s, info);
-        case kModeVpBwd:
-          return launch_ring<T, 1, kModeVpBwd, 2>(a, a.V, nslots, ring_bytes, s, info);
+      if (ring_ok) {  // the ring kernel needs 16-B aligned rows
+        switch (mode) {
+          case kModeFwd: return launch_ring<T, 1, kModeFwd, 2>(a, a.V, nslots, ring_bytes, s, info);
+          case kModeVpStats:
+            return launch_ring<T, 1, kModeVpStats, 2>(a, a.V, nslots, ring_bytes, s, info);
+          case kModeVpBwd:
+            return launch_ring<T, 1, kModeVpBwd, 2>(a, a.V, nslots, ring_bytes, s, info);
+        }
       }
     }
   }

@@ -170,8 +170,12 @@ def test_token_weights(tm, orc, norm_mode):
 # ---------------------------------------------------------------------------- a1
 @pytest.mark.parametrize("dtype,V,T,generic", [("bf16", 151936, 40, False), ("bf16", 151936, 40, True),
                                                ("f32", 32000, 64, False), ("bf16", 1001, 33, False),
-                                               ("f32", 151936, 9, False), ("bf16", 8, 5, False)])
+                                               ("f32", 151936, 9, False), ("bf16", 8, 5, False),
+                                               ("bf16", 50257, 37, False), ("f32", 32001, 21, False),
+                                               ("bf16", 13, 7, False)])
 def test_logprob_fwd(tm, orc, dtype, V, T, generic):
+    """bf16 1001 / 50257 / 13 and f32 32001 rows start off 16-B boundaries:
+    the streaming kernel runs them in sector coordinates."""
     lens = [T]
     prob = orc.synth_problem(100 + V % 97, lens, V, dtype)
     logits = to_dev_logits(prob)
@@ -181,6 +185,21 @@ def test_logprob_fwd(tm, orc, dtype, V, T, generic):
         torch.cuda.synchronize()
     finally:
         tm.set_force_generic(False)
+    olp, oent, olse = orc.logprob_fwd(prob["logits"], prob["targets"])
+    assert_close(logp.cpu().numpy(), olp, what="logp")
+    assert_close(ent.cpu().numpy(), oent, what="entropy")
+    assert_close(lse.cpu().numpy(), olse, what="lse")
+
+
+def test_logprob_fwd_odd_stride_uses_streaming_kernel(tm, orc):
+    prob = orc.synth_problem(5, [45], 4099, "bf16")
+    T, V = 45, 4099
+    base = torch.zeros(T, V + 5, dtype=torch.bfloat16, device="cuda")
+    view = base[:, 3:3 + V]
+    view.copy_(to_dev_logits(prob))
+    logp, ent, lse = tm.logprob_fwd(view, i32(prob["targets"]))
+    torch.cuda.synchronize()
+    assert tm.handle().last_launch()["kernel"] == "fwd_stream_kernel"
     olp, oent, olse = orc.logprob_fwd(prob["logits"], prob["targets"])
     assert_close(logp.cpu().numpy(), olp, what="logp")
     assert_close(ent.cpu().numpy(), oent, what="entropy")
