@@ -153,6 +153,20 @@ int sf_tm_logprob_fwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, i
                       int64_t ld, const int32_t* targets, float inv_temperature, float* out_logp,
                       float* out_entropy, float* out_lse, void* stream);
 
+/* Host-buffer forms for the stage seams (include/staleflow/train_math_seam.hpp):
+ * ActorFwd / RefLogP put a `logp` / `ref_logp` payload per sample
+ * (proj/src/sim_runtime.cpp:322-334, proj/src/wall_runtime.cpp:126-129) and the
+ * Advantages stage an `advantage` (controller.cpp:79). Inputs and outputs are
+ * host arrays (pinned for asynchronous copies); logits stay on the device.
+ * Results are valid once `stream` is synchronised. */
+/* Blocks until all work queued on `stream` (by this library or not) is done. */
+int sf_tm_sync(sf_tm_t h, void* stream);
+int sf_tm_logprob_fwd_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,
+                           const int32_t* h_targets, float inv_temperature, float* h_logp, float* h_entropy,
+                           void* stream);
+int sf_tm_grpo_advantage_host(sf_tm_t h, const float* h_rewards, const int32_t* h_group_ids, int64_t B, float eps,
+                              int32_t std_mode, float* h_adv, void* stream);
+
 /* ---- a4 prologue: per-token advantage and loss weight --------------------
  * From cu_seqlens[B+1], adv_seq[B], mask[T] (u8, NULL = all active):
  * out_adv_tok[T] = adv_seq[seq(t)], out_w_tok[T] = mask_t * inv_norm_t. */

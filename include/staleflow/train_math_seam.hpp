@@ -262,5 +262,169 @@ class ActorLossSeam {
   size_t pin_cap_[7] = {0, 0, 0, 0, 0, 0, 0};
 };
 
+// Pinned staging buffers, grown on demand and reused (used by the seams below).
+class PinnedStage {
+ public:
+  PinnedStage() = default;
+  PinnedStage(const PinnedStage&) = delete;
+  PinnedStage& operator=(const PinnedStage&) = delete;
+  ~PinnedStage() {
+    for (auto& b : buf_)
+      if (b.p) sf_tm_host_free(b.p);
+  }
+  // Returns a pinned buffer of >= bytes for slot i (contents not preserved).
+  void* get(int i, size_t bytes, int* rc) {
+    if (static_cast<size_t>(i) >= buf_.size()) buf_.resize(i + 1);
+    Buf& b = buf_[i];
+    if (b.cap < bytes) {
+      if (b.p) sf_tm_host_free(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+      const size_t cap = bytes + bytes / 4 + 64;
+      if ((*rc = sf_tm_host_alloc(cap, &b.p)) != SF_TM_OK) return nullptr;
+      b.cap = cap;
+    }
+    *rc = SF_TM_OK;
+    return b.p;
+  }
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Buf> buf_;
+};
+
+// ActorFwd / RefLogP stage producer (the payload stub at proj/src/sim_runtime.cpp:322-334,
+// proj/src/wall_runtime.cpp:126-129): the per-sample `logp` (or `ref_logp`) payload,
+// fp32[L_i] = log-prob of each response token under the stage model, from that
+// model's device logits [T, V] (samples concatenated in bus order). Synchronous:
+// `payloads[i]` is ready for Bus::put_field when run returns.
+class LogpStageSeam {
+ public:
+  explicit LogpStageSeam(int device = 0) { rc_ = sf_tm_create(device, &h_); }
+  ~LogpStageSeam() {
+    if (h_) sf_tm_destroy(h_);
+  }
+  LogpStageSeam(const LogpStageSeam&) = delete;
+  LogpStageSeam& operator=(const LogpStageSeam&) = delete;
+  int status() const { return rc_; }
+  sf_tm_t handle() const { return h_; }
+  const std::string& error() const { return err_; }
+
+  template <class MicroBatchT, class BytesT>
+  int run(const MicroBatchT& b, const void* d_logits, int32_t dtype, int64_t V, float inv_temperature,
+          std::vector<BytesT>& payloads, void* stream) {
+    if (rc_ != SF_TM_OK) return rc_;
+    const int jr = detail::find_field(b.field_set, "response");
+    if (jr < 0 || b.payloads.size() != b.sample_ids.size()) {
+      err_ = "the stage needs the response field with payloads";
+      return SF_TM_CONFIG_ERROR;
+    }
+    int64_t T = 0;
+    for (const auto& row : b.payloads) {
+      if (row[jr].size() % sizeof(int32_t)) {
+        err_ = "response payload is not int32[L]";
+        return SF_TM_CONFIG_ERROR;
+      }
+      T += static_cast<int64_t>(row[jr].size() / sizeof(int32_t));
+    }
+    int rc = SF_TM_OK;
+    auto* tg = static_cast<uint8_t*>(pin_.get(0, static_cast<size_t>(T) * 4 + 4, &rc));
+    if (rc) return rc;
+    auto* lp = static_cast<float*>(pin_.get(1, static_cast<size_t>(T) * 4 + 4, &rc));
+    if (rc) return rc;
+    size_t off = 0;
+    for (const auto& row : b.payloads) {
+      if (!row[jr].empty()) std::memcpy(tg + off, row[jr].data(), row[jr].size());
+      off += row[jr].size();
+    }
+    if ((rc = sf_tm_logprob_fwd_host(h_, d_logits, dtype, T, V, V, reinterpret_cast<const int32_t*>(tg),
+                                     inv_temperature, lp, nullptr, stream)) ||
+        (rc = sf_tm_sync(h_, stream))) {
+      err_ = sf_tm_last_error(h_);
+      return rc;
+    }
+    payloads.assign(b.payloads.size(), BytesT{});
+    off = 0;
+    for (size_t i = 0; i < b.payloads.size(); ++i) {
+      const size_t L = b.payloads[i][jr].size() / sizeof(int32_t);
+      payloads[i].resize(L * sizeof(float));
+      if (L) std::memcpy(payloads[i].data(), lp + off, L * sizeof(float));
+      off += L;
+    }
+    return SF_TM_OK;
+  }
+
+ private:
+  sf_tm_t h_ = nullptr;
+  int rc_ = SF_TM_OK;
+  std::string err_;
+  PinnedStage pin_;
+};
+
+// Advantages stage producer (controller.cpp:79 reward -> advantage): GRPO over
+// the micro-batch's groups (field `group`, else (sample_id - 1) / group_size);
+// every group must be complete. payloads[i] = fp32 advantage.
+class AdvantageStageSeam {
+ public:
+  explicit AdvantageStageSeam(int device = 0) { rc_ = sf_tm_create(device, &h_); }
+  ~AdvantageStageSeam() {
+    if (h_) sf_tm_destroy(h_);
+  }
+  AdvantageStageSeam(const AdvantageStageSeam&) = delete;
+  AdvantageStageSeam& operator=(const AdvantageStageSeam&) = delete;
+  int status() const { return rc_; }
+  const std::string& error() const { return err_; }
+
+  template <class MicroBatchT, class BytesT>
+  int run(const MicroBatchT& b, int group_size, float eps, int32_t std_mode, std::vector<BytesT>& payloads,
+          void* stream) {
+    if (rc_ != SF_TM_OK) return rc_;
+    const int jw = detail::find_field(b.field_set, "reward"), jg = detail::find_field(b.field_set, "group");
+    if (jw < 0 || b.payloads.size() != b.sample_ids.size() || (jg < 0 && group_size <= 0)) {
+      err_ = "the stage needs the reward field with payloads and a group field or group_size";
+      return SF_TM_CONFIG_ERROR;
+    }
+    const int64_t B = static_cast<int64_t>(b.sample_ids.size());
+    PackedBatch p;
+    for (int64_t i = 0; i < B; ++i) {
+      const auto& row = b.payloads[i];
+      if (!detail::append(row[jw], p.per_sample, 1) || (jg >= 0 && !detail::append(row[jg], p.group_ids, 1))) {
+        err_ = "sample " + std::to_string(b.sample_ids[i]) + ": reward/group payload is not 4 bytes";
+        return SF_TM_CONFIG_ERROR;
+      }
+      if (jg < 0) p.group_ids.push_back(static_cast<int32_t>((b.sample_ids[i] - 1) / group_size));
+    }
+    int rc = check_complete_groups(p, jg < 0 ? group_size : 0, &err_);
+    if (rc) return rc;
+    auto* rw = static_cast<float*>(pin_.get(0, static_cast<size_t>(B) * 4 + 4, &rc));
+    if (rc) return rc;
+    auto* gi = static_cast<int32_t*>(pin_.get(1, static_cast<size_t>(B) * 4 + 4, &rc));
+    if (rc) return rc;
+    auto* ad = static_cast<float*>(pin_.get(2, static_cast<size_t>(B) * 4 + 4, &rc));
+    if (rc) return rc;
+    if (B) {
+      std::memcpy(rw, p.per_sample.data(), static_cast<size_t>(B) * 4);
+      std::memcpy(gi, p.group_ids.data(), static_cast<size_t>(B) * 4);
+    }
+    if ((rc = sf_tm_grpo_advantage_host(h_, rw, gi, B, eps, std_mode, ad, stream)) ||
+        (rc = sf_tm_sync(h_, stream))) {
+      err_ = sf_tm_last_error(h_);
+      return rc;
+    }
+    payloads.assign(static_cast<size_t>(B), BytesT(sizeof(float)));
+    for (int64_t i = 0; i < B; ++i) std::memcpy(payloads[i].data(), ad + i, sizeof(float));
+    return SF_TM_OK;
+  }
+
+ private:
+  sf_tm_t h_ = nullptr;
+  int rc_ = SF_TM_OK;
+  std::string err_;
+  PinnedStage pin_;
+};
+
 }  // namespace train_math
 }  // namespace staleflow

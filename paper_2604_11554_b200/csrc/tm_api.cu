@@ -162,6 +162,31 @@ int run_rows(sf_tm_t h, sftm::RowArgs& a, int mode, cudaStream_t s, const char* 
 
 }  // namespace
 
+namespace {
+// Grow-once host-call scratch (per-token and per-sample device buffers).
+int ensure_tscratch(sf_tm_t h, int64_t T) {
+  if (T <= h->tcap) return SF_TM_OK;
+  int rc = 0;
+  if ((rc = grow(h, &h->d_targets, T, "scratch")) || (rc = grow(h, &h->d_old, T, "scratch")) ||
+      (rc = grow(h, &h->d_ref, T, "scratch")) || (rc = grow(h, &h->d_mask, T, "scratch")) ||
+      (rc = grow(h, &h->d_advtok, T, "scratch")) || (rc = grow(h, &h->d_wtok, T, "scratch")))
+    return rc;
+  h->tcap = T;
+  return SF_TM_OK;
+}
+int ensure_bscratch(sf_tm_t h, int64_t B) {
+  if (B <= h->bcap) return SF_TM_OK;
+  int rc = 0;
+  if ((rc = grow(h, &h->d_lens, B, "scratch")) || (rc = grow(h, &h->d_plens, B, "scratch")) ||
+      (rc = grow(h, &h->d_rewards, B, "scratch")) || (rc = grow(h, &h->d_gids, B, "scratch")) ||
+      (rc = grow(h, &h->d_cu, B + 1, "scratch")) || (rc = grow(h, &h->d_adv, B, "scratch")))
+    return rc;
+  h->bcap = B;
+  return SF_TM_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 void sf_tm_default_loss_params(sf_tm_loss_params* p) {
@@ -386,24 +411,8 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
   if (tsum != T) return fail(h, SF_TM_CONFIG_ERROR, "sum(seq_lens) != T");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // grow-once scratch
-  if (T > h->tcap) {
-    const int64_t c = T;
-    int rc = 0;
-    if ((rc = grow(h, &h->d_targets, c, "scratch")) || (rc = grow(h, &h->d_old, c, "scratch")) ||
-        (rc = grow(h, &h->d_ref, c, "scratch")) || (rc = grow(h, &h->d_mask, c, "scratch")) ||
-        (rc = grow(h, &h->d_advtok, c, "scratch")) || (rc = grow(h, &h->d_wtok, c, "scratch")))
-      return rc;
-    h->tcap = c;
-  }
-  if (B > h->bcap) {
-    const int64_t c = B;
-    int rc = 0;
-    if ((rc = grow(h, &h->d_lens, c, "scratch")) || (rc = grow(h, &h->d_plens, c, "scratch")) ||
-        (rc = grow(h, &h->d_rewards, c, "scratch")) || (rc = grow(h, &h->d_gids, c, "scratch")) ||
-        (rc = grow(h, &h->d_cu, c + 1, "scratch")) || (rc = grow(h, &h->d_adv, c, "scratch")))
-      return rc;
-    h->bcap = c;
-  }
+  if (int rc = ensure_tscratch(h, T)) return rc;
+  if (int rc = ensure_bscratch(h, B)) return rc;
   if (int rc = ensure_cnt(h, B)) return rc;
   auto h2d = [&](void* d, const void* src, size_t bytes) {
     return cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s);
@@ -463,6 +472,66 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
   e = cudaMemcpyAsync(h_metrics, h->d_metrics, sizeof(float) * SF_TM_NUM_METRICS,
                       cudaMemcpyDeviceToHost, s);
   return check_cuda(h, e, "sf_tm_pg_step_host D2H");
+}
+
+int sf_tm_sync(sf_tm_t h, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  return check_cuda(h, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sf_tm_sync");
+}
+
+int sf_tm_logprob_fwd_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,
+                           const int32_t* h_targets, float inv_temperature, float* h_logp, float* h_entropy,
+                           void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (int rc = check_rows(h, logits, dtype, T, V, ld, h_targets)) return rc;
+  if (!(inv_temperature > 0.f && std::isfinite(inv_temperature)))
+    return fail(h, SF_TM_CONFIG_ERROR, "inv_temperature must be > 0");
+  if (T == 0) return SF_TM_OK;
+  if (!h_logp) return fail(h, SF_TM_CONFIG_ERROR, "h_logp is required");
+  if (int rc = ensure_tscratch(h, T)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(h->d_targets, h_targets, sizeof(int32_t) * T, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sf_tm_logprob_fwd_host H2D");
+  sftm::RowArgs a;
+  a.logits = logits;
+  a.dtype = dtype;
+  a.T = T;
+  a.V = V;
+  a.ld = ld;
+  a.targets = h->d_targets;
+  a.inv_tau = inv_temperature;
+  a.out_logp = h->d_old;
+  a.out_entropy = h_entropy ? h->d_ref : nullptr;
+  if (int rc = run_rows(h, a, sftm::kModeFwd, s, "sf_tm_logprob_fwd_host")) return rc;
+  e = cudaMemcpyAsync(h_logp, h->d_old, sizeof(float) * T, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && h_entropy)
+    e = cudaMemcpyAsync(h_entropy, h->d_ref, sizeof(float) * T, cudaMemcpyDeviceToHost, s);
+  return check_cuda(h, e, "sf_tm_logprob_fwd_host D2H");
+}
+
+int sf_tm_grpo_advantage_host(sf_tm_t h, const float* h_rewards, const int32_t* h_group_ids, int64_t B, float eps,
+                              int32_t std_mode, float* h_adv, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (B < 0) return fail(h, SF_TM_CONFIG_ERROR, "B must be >= 0");
+  if (std_mode < 0 || std_mode > 2) return fail(h, SF_TM_CONFIG_ERROR, "std_mode must be SF_TM_STD_*");
+  if (!(eps >= 0.f && std::isfinite(eps))) return fail(h, SF_TM_CONFIG_ERROR, "eps must be >= 0");
+  if (B == 0) return SF_TM_OK;
+  if (!h_rewards || !h_group_ids || !h_adv)
+    return fail(h, SF_TM_CONFIG_ERROR, "h_rewards, h_group_ids and h_adv are required");
+  if (int rc = ensure_bscratch(h, B)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(h->d_rewards, h_rewards, sizeof(float) * B, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->d_gids, h_group_ids, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sf_tm_grpo_advantage_host H2D");
+  int n = 0;
+  const int rc = sftm::launch_grpo_advantage(h->d_rewards, h->d_gids, B, eps, std_mode, h->d_adv, nullptr, s, &n);
+  h->launches += n;
+  if (rc) return cuda_fail(h, rc, "sf_tm_grpo_advantage_host");
+  e = cudaMemcpyAsync(h_adv, h->d_adv, sizeof(float) * B, cudaMemcpyDeviceToHost, s);
+  return check_cuda(h, e, "sf_tm_grpo_advantage_host D2H");
 }
 
 int sf_tm_r3_gate_fwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64_t L, int64_t T,

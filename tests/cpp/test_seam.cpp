@@ -4,6 +4,7 @@
 //                      staleflow::MicroBatch when built with -DSF_USE_REF_TYPES)
 //   ./test_seam gpu    B200: ActorLossSeam::step == sf_tm_pg_step_host on the same
 //                      packed arrays (bitwise metrics and dlogits)
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -228,6 +229,59 @@ void test_gpu() {
     cudaFree(rec_d);
     cudaFree(w);
     cudaFree(idx);
+  }
+  // stage producers: ActorFwd/RefLogP logp payloads and the Advantages stage
+  {
+    MicroBatch sb = make_batch(V, 6, 120, 21, false);  // fields logp, ref_logp, response, reward
+    staleflow::train_math::PackedBatch sp;
+    staleflow::train_math::pack_trainer_batch(sb, 3, sp, &err);
+    void* lg = nullptr;
+    cudaMalloc(&lg, sp.T * V * 2);
+    staleflow::train_math::LogpStageSeam st(0);
+    CHECK(sf_tm_synth_logits(st.handle(), lg, SF_TM_BF16, sp.T, V, V, 8, 2.f, nullptr, 0.f, 0.f, 1e-3f, nullptr) ==
+          SF_TM_OK);
+    std::vector<Bytes> lp_payloads;
+    CHECK(st.run(sb, lg, SF_TM_BF16, V, 1.f, lp_payloads, nullptr) == SF_TM_OK);
+    CHECK(lp_payloads.size() == 6);
+    // same numbers as the device-buffer C-ABI call
+    int32_t* dt = nullptr;
+    float* dl = nullptr;
+    cudaMalloc(&dt, sp.T * 4);
+    cudaMalloc(&dl, sp.T * 4);
+    cudaMemcpy(dt, sp.targets.data(), sp.T * 4, cudaMemcpyHostToDevice);
+    CHECK(sf_tm_logprob_fwd(st.handle(), lg, SF_TM_BF16, sp.T, V, V, dt, 1.f, dl, nullptr, nullptr, nullptr) == SF_TM_OK);
+    std::vector<float> ref(sp.T);
+    cudaMemcpy(ref.data(), dl, sp.T * 4, cudaMemcpyDeviceToHost);
+    size_t off = 0;
+    bool same = true;
+    for (size_t i = 0; i < lp_payloads.size(); ++i) {
+      same &= lp_payloads[i].size() == static_cast<size_t>(sp.seq_lens[i]) * 4;
+      same &= std::memcmp(lp_payloads[i].data(), ref.data() + off, lp_payloads[i].size()) == 0;
+      off += sp.seq_lens[i];
+    }
+    CHECK(same);
+    cudaFree(lg);
+    cudaFree(dt);
+    cudaFree(dl);
+    staleflow::train_math::AdvantageStageSeam av(0);
+    std::vector<Bytes> adv_payloads;
+    CHECK(av.run(sb, 3, 1e-6f, SF_TM_STD_UNBIASED, adv_payloads, nullptr) == SF_TM_OK);
+    bool ok = adv_payloads.size() == 6;
+    for (int g = 0; g < 2 && ok; ++g) {
+      double m = 0, v = 0;
+      for (int j = 0; j < 3; ++j) m += sp.per_sample[3 * g + j];
+      m /= 3;
+      for (int j = 0; j < 3; ++j) v += (sp.per_sample[3 * g + j] - m) * (sp.per_sample[3 * g + j] - m);
+      const double sd = std::sqrt(v / 2);
+      for (int j = 0; j < 3; ++j) {
+        float a;
+        std::memcpy(&a, adv_payloads[3 * g + j].data(), 4);
+        const double want = sd == 0 ? 0.0 : (sp.per_sample[3 * g + j] - m) / (sd + 1e-6);
+        ok &= std::fabs(a - want) <= 1e-5 * (1 + std::fabs(want));
+      }
+    }
+    CHECK(ok);
+    CHECK(av.run(sb, 4, 1e-6f, SF_TM_STD_UNBIASED, adv_payloads, nullptr) == SF_TM_CONFIG_ERROR);  // 6 % 4: incomplete
   }
   std::printf(fails ? "GPU FAILED\n" : "GPU OK loss=%g active=%g\n", m1[0], m1[SF_TM_M_ACTIVE]);
 }
