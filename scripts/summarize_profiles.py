@@ -80,6 +80,47 @@ def full(tag):
     return "\n".join(md)
 
 
+EXTRA = [  # (capture name in gpurun_out, what, command)
+    ("r1_fwd_stream", "forward-only streaming kernel (a1), 131,072 x 151,936 bf16",
+     "scripts/ncu_kernel.sh r1_fwd_stream fwd_stream_kernel 3 python scripts/fwd_only.py"),
+    ("r1_r3_fwd", "R3 gate forward, 48 x 131,072 rows x 128 experts fp32, top-8",
+     "scripts/ncu_kernel.sh r1_r3_fwd r3_fwd_fast 3 python scripts/r3_split.py"),
+]
+
+
+def extra(tag):
+    md = []
+    for name, what, cmd in EXTRA:
+        rep = os.path.join(OUT, f"{name}.ncu-rep")
+        dst = os.path.join(PROF, f"{name}.ncu-rep")
+        if os.path.exists(rep):
+            shutil.copy(rep, dst)
+        if not os.path.exists(dst):
+            continue
+        raw = ncu_raw(dst)
+        keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
+        md += ["", f"# {tag}: `ncu --set full` of the {what}", "", f"Command: `{cmd}`; report `profiles/{name}.ncu-rep`.",
+               "", "| metric | value |", "|---|---|"]
+        for k in keys:
+            if k in raw:
+                u, v = raw[k]
+                md.append(f"| `{k}` | {v} {u} |")
+        if "dram__bytes_read.sum" in raw and "gpu__time_duration.sum" in raw:
+            def num(k):
+                u, v = raw[k]
+                f = float(v.replace(",", ""))
+                return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1e-3, "us": 1e-6,
+                            "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "nsecond": 1e-9}.get(u, 1)
+            gbs = (num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) / num("gpu__time_duration.sum") / 1e9
+            md.append(f"| DRAM GB/s (read+write / duration) | {gbs:.0f} |")
+    return "\n".join(md)
+
+
 def traffic(tag):
     lines = [l for l in open(os.path.join(OUT, "ev_traffic.csv")) if not l.startswith("==")]
     rows = list(csv.DictReader(io.StringIO("".join(lines))))
@@ -98,7 +139,7 @@ def traffic(tag):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
     os.makedirs(PROF, exist_ok=True)
-    parts = [launches(tag), "", full(tag)]
+    parts = [launches(tag), "", full(tag), extra(tag)]
     t = traffic(tag)
     parts += ["", f"# {tag}: DRAM traffic of one headline launch (131,072 rows x 151,936 bf16)", "",
               f"read {t['dram_bytes_read'] / 1e9:.3f} GB + write {t['dram_bytes_write'] / 1e9:.3f} GB = "
