@@ -6,28 +6,36 @@
 // logits row is read once and its gradient written once (4V bytes per
 // loss-active bf16 token).
 //
-// sm_100a structure (one CTA per SM, a C-CTA cluster per row, persistent):
+// sm_100a structure (one CTA per SM, persistent, rows grid-strided; a row is
+// split over a C-CTA cluster only when one CTA's slice would not fit the row
+// store):
 //
-//   warp 16        TMA producer: cp.async.bulk 8 KB chunks of this CTA's row
-//                  slice into a 26-slot shared-memory ring (mbarrier
-//                  complete_tx), running ahead across rows.
-//   warps 0..7     FORWARD: read a chunk from smem, release the smem slot at
-//                  once, stash the raw words in TENSOR MEMORY (tcgen05.st,
-//                  32 slots x 8 KB = the whole 256 KB TMEM) and fold them into
-//                  the online (max, sum, weighted-sum) softmax state. At the
-//                  end of a row: CTA reduction, then the partial statistics go
-//                  to every CTA of the cluster through DSMEM mailboxes with
-//                  remote mbarrier arrives.
-//   warps 8..15    BACKWARD: wait for the row's merged statistics, compute the
-//                  per-token loss scalars, then re-read the row from TMEM
-//                  (tcgen05.ld), form dlogits and stream them to HBM.
+//   warp 24        TMA producer: cp.async.bulk 12 KB chunks of the row slice
+//                  into an 8-slot smem ring (mbarrier complete_tx), L2
+//                  evict-first, running ahead across rows.
+//   warps 12..23   FORWARD: read a chunk (2 x LDS.128 per thread), copy it into
+//                  the ROW STORE, release the ring slot, and fold it into the
+//                  online softmax state (fixed per-thread exponent base, packed
+//                  FFMA2/FADD2, MUFU.EX2). Row end: warp merge, per-warp partial
+//                  into a flow-controlled smem ring.
+//   warps 25,26    CONTROL (alternating rows): merge the 12 partials, exchange
+//                  them with the cluster (DSMEM mailboxes) or, in the XP
+//                  instantiation, with the other GPUs (peer-memory mailboxes;
+//                  then warp 25 sends and warp 26 receives), compute the loss
+//                  scalars once, publish them to the backward warps; metrics
+//                  accumulate in fp64.
+//   warps 0..11    BACKWARD: wait for the row's scalars, re-read the row from
+//                  the row store, form dlogits (bf16: |c0| folded into the
+//                  exponent, the sign XOR-ed onto packed words), 16-B streaming
+//                  stores.
 //
-// TMEM is the row store that makes single-pass possible: a Qwen3 bf16 row
-// (303,872 B) split over a 2-CTA cluster is 152 KB per SM, which fits TMEM
-// with 13 chunks of slack, so the forward warps run up to ~0.7 rows ahead of
-// the backward warps and both overlap the TMA stream. Each backward warp reads
-// exactly the TMEM lanes/columns its partner forward warp (same SM
-// sub-partition, warp b = f + 8) wrote, so TMEM needs no cross-lane layout.
+// The row store is TMEM (21 slots of 24 columns, tcgen05.st/ld.32x32b.x8)
+// followed by 10 smem slots: 31 x 12 KB, a whole Qwen3 bf16 row (25 chunks) and
+// part of the next, so forward(r+1) overlaps backward(r) and every row is read
+// from HBM exactly once. Each backward warp reads exactly the TMEM lanes/columns
+// its partner forward warp (same SM sub-partition) wrote. Every slot is
+// released only after the values read from it fed a dependent instruction
+// (SASS issues an mbarrier arrive right behind an LDS without waiting for it).
 //
 // Reference seam replaced: trainer_compute_batch latency (proj/src/sim_runtime.cpp:441)
 // and trainer_thread sleep (proj/src/wall_runtime.cpp:197); math pinned in

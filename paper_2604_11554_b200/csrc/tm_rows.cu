@@ -1,26 +1,20 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// Vocab-row kernels of the train-math hot path:
+// Vocab-row kernels of the train-math hot path
+// and the dispatch that picks one per call (launch_rows, bottom of this file):
 //
-//   rows_ring_kernel   — the sm_100a path. One producer warp streams each CTA's
-//                        slice of a logits row into a shared-memory ring with TMA
-//                        1-D bulk copies (cp.async.bulk + mbarrier complete_tx);
-//                        16 compute warps run the online (max, sum, weighted-sum)
-//                        softmax over it. In the fused loss mode (kModeFwdBwd) the
-//                        row is split over a C-CTA thread-block cluster so that
-//                        each CTA's slice stays RESIDENT in smem between the
-//                        forward statistics and the dlogits backward: the row is
-//                        read from HBM exactly once and dlogits written once
-//                        (4V bytes/token for bf16). Per-CTA partial statistics
-//                        are exchanged through DSMEM mailboxes with remote
-//                        mbarrier arrives (no cluster-wide barrier per row).
-//                        Ring slots are released as soon as the backward has
-//                        consumed them, so the next row's TMA loads overlap the
-//                        current row's dlogits stores.
-//   rows_generic_kernel — fallback for shapes the ring cannot take (unaligned
-//                        rows/strides, vocabularies too wide for an 8-CTA
-//                        cluster): two passes over global memory (the second
-//                        served from L2), same math, same outputs.
+//   loss_tmem_kernel (tm_loss.cu)  — fused loss fwd+bwd (kModeFwdBwd), any
+//                        element-aligned rows (16-B aligned, or in sector
+//                        coordinates when not) whose slice fits the row store.
+//   fwd_stream_kernel (tm_fwd.cu)  — forward only (kModeFwd, kModeVpStats).
+//   rows_ring_kernel   — a TMA-ring streaming kernel with 16 compute warps: the
+//                        two-pass vocab-parallel shard backward (kModeVpBwd), and
+//                        the A/B baseline for the forward modes (SFTM_FWD_RING=1).
+//   rows_generic_kernel — fallback for what the above cannot take (dlogits at a
+//                        different 16-B phase than the logits, rows too wide
+//                        for any row store, unaligned rows in kModeVpBwd): two
+//                        passes over global memory (the second served from L2),
+//                        same math, same outputs.
 //
 // The per-row math (lse, entropy, logp, DAPO/GRPO surrogate, k3 KL, gradients)
 // is pinned in DESIGN.md §2 and restated in fp64 by oracle/sf_oracle.c
