@@ -1018,10 +1018,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (j == jt) gr[j] += gt;
           }
         } else {
+          // entropy term: -p_v (c0 + c1 a_v); the clamp keeps a -inf logit at 0 (not NaN)
+          const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2, -lse2);
+          const float2 mc1 = make_float2(-c1, -c1), mc0 = make_float2(-c0, -c0);
 #pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const float av = fmaxf(fmaf(x[j], c, -lse2), -127.f);
-            gr[j] = -ex2(av) * fmaf(c1, av, c0);
+          for (int p = 0; p < NE / 2; ++p) {
+            float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+            av.x = fmaxf(av.x, -127.f);
+            av.y = fmaxf(av.y, -127.f);
+            const float2 t2 = __ffma2_rn(mc1, av, mc0);
+            const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), t2);
+            gr[2 * p] = g2.x;
+            gr[2 * p + 1] = g2.y;
           }
           if (k == ck) {
 #pragma unroll
