@@ -312,8 +312,8 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     h = tm.handle(dev.index)
 
     fused = not args.vp_two_pass
-    if fused and P > 1:
-        open_peer_exchange()
+    if fused and P > 1 and not open_peer_exchange():
+        fused = False  # no P2P path between the ranks: the two-pass NCCL form
 
     def step(rec):
         ev = []

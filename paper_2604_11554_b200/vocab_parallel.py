@@ -73,26 +73,49 @@ def vp_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp,
 _peer_groups: dict = {}
 
 
-def open_peer_exchange(group=None) -> None:
+def open_peer_exchange(group=None) -> bool:
     """Create this rank's peer mailbox, all-gather the 64-byte CUDA IPC handles
-    over `group` (any backend) and map the peers. Idempotent per device."""
+    over `group` (any backend) and map the peers. The outcome is agreed on by
+    all ranks: if any rank cannot map its peers (no P2P path), every rank
+    reports False and the callers use the two-pass NCCL form. Idempotent per
+    device."""
     dev = torch.cuda.current_device()
     if dev in _peer_groups:
-        return
+        return _peer_groups[dev]
     P = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    mine = tm.vp_mailbox_create(P, rank, dev)
+    ok = True
     handles = [None] * P
+    try:
+        mine = tm.vp_mailbox_create(P, rank, dev)
+    except tm.TrainMathError:
+        mine, ok = None, False
     dist.all_gather_object(handles, mine, group=group)
-    tm.vp_mailbox_open(handles, dev)
-    _peer_groups[dev] = (P, rank)
+    if ok and all(h is not None for h in handles):
+        try:
+            tm.vp_mailbox_open(handles, dev)
+        except tm.TrainMathError:
+            ok = False
+    else:
+        ok = False
+    flags = [None] * P
+    dist.all_gather_object(flags, ok, group=group)
+    _peer_groups[dev] = all(flags)
+    return _peer_groups[dev]
 
 
 def vp_fused_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
                              params: Optional[LossParams] = None, dlogits=None, group=None, want_logp: bool = False,
                              metrics=None):
     """Single-pass vocab-parallel fused loss (exchange inside the kernel over
-    NVLink peer memory); same outputs as vp_pg_loss_fwd_bwd."""
-    open_peer_exchange(group)
+    NVLink peer memory); same outputs as vp_pg_loss_fwd_bwd, which it falls back
+    to (on every rank) when the ranks cannot map each other's memory."""
+    if not open_peer_exchange(group):
+        met, dl, lp, ent = vp_pg_loss_fwd_bwd(shard, vocab_start, targets, old_logp, ref_logp, adv_tok, w_tok, params,
+                                              dlogits=dlogits, group=group, want_logp=want_logp)
+        if metrics is not None:
+            metrics.copy_(met)
+            met = metrics
+        return met, dl, lp, ent
     return tm.vp_fused_loss_fwd_bwd(shard, vocab_start, targets, old_logp, ref_logp, adv_tok, w_tok, params,
                                     dlogits=dlogits, want_logp=want_logp, metrics=metrics)
