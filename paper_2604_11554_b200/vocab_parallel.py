@@ -79,7 +79,7 @@ def open_peer_exchange(group=None) -> bool:
     all ranks: if any rank cannot map its peers (no P2P path), every rank
     reports False and the callers use the two-pass NCCL form. Idempotent per
     device."""
-    dev = torch.cuda.current_device()
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
     if dev in _peer_groups:
         return _peer_groups[dev]
     P = dist.get_world_size(group)

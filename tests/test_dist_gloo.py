@@ -95,6 +95,50 @@ def test_two_rank_gloo_protocols():
         assert ok_dp, f"sequence-shard metric all-reduce mismatch on rank {rank}"
 
 
+def _agree_worker(rank, world, port, q, fail_rank):
+    """open_peer_exchange's collective decision with a (mocked) mailbox layer:
+    one rank failing to map its peers makes every rank fall back."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_11554_b200 import train_math as tm
+        from paper_2604_11554_b200 import vocab_parallel as vp
+
+        opened = []
+        tm.vp_mailbox_create = lambda P, r, dev=None: bytes([r]) * 64
+        def _open(handles, dev=None):
+            if rank == fail_rank:
+                raise tm.TrainMathError(26, "no peer access (mock)")
+            opened.append(len(handles))
+        tm.vp_mailbox_open = _open
+        ok = vp.open_peer_exchange()
+        again = vp.open_peer_exchange()  # idempotent, no second exchange
+        q.put((rank, ok, again, opened))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_peer_exchange_agreement(fail_rank):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = fail_rank < 0
+    for rank, ok, again, opened in res:
+        assert ok is want and again is want, (rank, ok, again)
+        if rank != fail_rank:
+            assert opened == [world]
+
+
 def test_shard_bounds():
     from paper_2604_11554_b200.vocab_parallel import shard_bounds
 
