@@ -18,10 +18,10 @@
 //                  online softmax state (fixed per-thread exponent base, packed
 //                  FFMA2/FADD2, MUFU.EX2). Row end: warp merge, per-warp partial
 //                  into a flow-controlled smem ring.
-//   warps 25,26    CONTROL (alternating rows): merge the 12 partials, exchange
+//   warps 25..27   CONTROL (rotating rows): merge the 12 partials, exchange
 //                  them with the cluster (DSMEM mailboxes) or, in the XP
 //                  instantiation, with the other GPUs (peer-memory mailboxes;
-//                  then warp 25 sends and warp 26 receives), compute the loss
+//                  then warp 25 sends and warps 26, 27 receive), compute the loss
 //                  scalars once, publish them to the backward warps; metrics
 //                  accumulate in fp64.
 //   warps 0..11    BACKWARD: wait for the row's scalars, re-read the row from
@@ -59,10 +59,11 @@ constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
 constexpr int kCtl = kFW + kBW + 1;         // control warps (2, alternating rows): merge, exchange, scalars
 #ifndef SFTM_NCTL
-#define SFTM_NCTL 2
+#define SFTM_NCTL 3
 #endif
 constexpr int kNCtl = SFTM_NCTL;
-constexpr int kThreads = (kFW + kBW + 1 + kNCtl) * 32;  // 864
+constexpr int kThreads = (kFW + kBW + 1 + kNCtl) * 32;  // 896
+static_assert(kNCtl >= 2, "the peer exchange needs a sender and at least one receiver warp");
 constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per thread = 12 KB
 #ifndef SFTM_RING_SLOTS
 #define SFTM_RING_SLOTS 8
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Per row: merge the 12 forward partials, exchange with the cluster through
     // DSMEM mailboxes, compute the loss scalars once and publish them to the
     // backward warps. Never touches the row data, so it runs as far ahead as
-    // the forward warps allow. Two control warps take alternating active rows
+    // the forward warps allow. The control warps take rotating active rows
     // so the per-row latency chain (merge -> DSMEM round trip -> scalars) of
     // one row overlaps the next.
     const int ci = warp - kCtl;
@@ -609,8 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Peer exchange: the latency of a cross-GPU round trip is several rows
       // long, so sending and receiving are split. Warp 0 (sender) merges the
       // forward partials and posts them to every rank's mailbox as soon as the
-      // row's forward is done; warp 1 (receiver) consumes the rows in order,
-      // merges the P partials in rank order and publishes the scalars. The
+      // row's forward is done; the receivers (the other control warps, rows
+      // alternating) merge the P partials in rank order and publish the scalars. The
       // sender stays at most kXpCredit rows ahead of the receiver, which with
       // the same bound on every rank keeps any rank from overrunning a peer's
       // kMailD-deep mailbox ring.
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (cid < a.T) {
         wn = __ldg(a.w_tok + cid);
         yn = __ldg(a.targets + cid);
-        if (ci == 1) {
+        if (ci >= 1) {
           An = __ldg(a.adv_tok + cid);
           oldn = __ldg(a.old_logp + cid);
           refn = __ldg(a.ref_logp + cid);
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t tn = t + ncl;
           wn = __ldg(a.w_tok + tn);
           yn = __ldg(a.targets + tn);
-          if (ci == 1) {
+          if (ci >= 1) {
             An = __ldg(a.adv_tok + tn);
             oldn = __ldg(a.old_logp + tn);
             refn = __ldg(a.ref_logp + tn);
@@ -671,8 +672,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             st_sys_v2u64(&dst->w[0], tag | __float_as_uint(v.m2), tag | __float_as_uint(v.s));
             st_sys_v2u64(&dst->w[2], tag | __float_as_uint(v.w), tag | __float_as_uint(zy));
           }
-        } else {
-          // ------------------------------------------------ receiver
+        } else if (static_cast<int>(nrow % (kNCtl - 1)) == ci - 1) {
+          // ------------------------------------------------ receivers (rows alternate)
           const uint32_t rs = nrow % kRD;
           const uint32_t rpar = (nrow / kRD) & 1u;
           const int64_t yl64 = yg - slice_start;
@@ -847,15 +848,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }  // XP / alternating
     // fixed-order combine of the two control warps' fp64 partials, then the
     // deterministic cross-block finish
-    __shared__ double acc_sh[8];
-    if (ci == 1 && lane == 0) {
+    __shared__ double acc_sh[kNCtl - 1][8];
+    if (ci >= 1 && lane == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc_sh[i] = acc[i];
+      for (int i = 0; i < 8; ++i) acc_sh[ci - 1][i] = acc[i];
     }
     named_bar_sync(2, kNCtl * 32);
     if (ci == 0 && leader) {
+      for (int q = 0; q < kNCtl - 1; ++q)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += acc_sh[i];
+        for (int i = 0; i < 8; ++i) acc[i] += acc_sh[q][i];
       finish_metrics(a, cid, ncl, acc);
     }
   } else {
