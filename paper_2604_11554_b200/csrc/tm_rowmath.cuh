@@ -121,8 +121,11 @@ __device__ __forceinline__ void loss_terms(float logp, float H, float w, float A
   const float d = ref - logp;
   const float er = expf(d);
   const float kl = er - d - 1.f;
-  const float gkl = P.beta * (1.f - er);
-  const float l = pg + P.beta * kl - P.ent * H;
+  // beta == 0 must drop the KL terms entirely: e^(ref - logp) overflows fp32 for
+  // rows the policy gives far less mass than the reference (0 * inf = NaN)
+  const bool has_kl = P.beta != 0.f;
+  const float gkl = has_kl ? P.beta * (1.f - er) : 0.f;
+  const float l = pg + (has_kl ? P.beta * kl : 0.f) - P.ent * H;
   g = w * (gpg + gkl);
   gH = -w * P.ent;
   m[0] = w * l;

@@ -321,6 +321,55 @@ def test_fused_all_rows_vs_streaming_forward(tm, dtype, T, V):
         assert int(bad.sum()) == 0, f"{int(bad.sum())} rows differ, e.g. {torch.nonzero(bad)[:5].flatten().tolist()}"
 
 
+@pytest.mark.parametrize("dtype,V,generic", [("f32", 8192, False), ("bf16", 20011, False), ("bf16", 151936, False),
+                                             ("f32", 8192, True)])
+def test_neg_inf_logits_and_exponent_overflow(tm, orc, dtype, V, generic):
+    """-inf logits (masked vocabulary entries), a row whose first chunk is far
+    below a later logit (the fixed exponent base overflows) and a row with a
+    single finite logit: the kernels' repair paths must match the oracle."""
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(31, [7, 6], V, "f32", prompt_max=0)
+    x = prob["logits"].copy()
+    rng = np.random.default_rng(3)
+    x[rng.random(x.shape) < 0.1] = -np.inf
+    x[0, :V // 2] = -100.0
+    x[0, V // 2 + 5] = 100.0
+    x[1, :] = -np.inf
+    x[1, 7] = 2.0
+    t = prob["targets"].copy()
+    t[1] = 7
+    for r in range(x.shape[0]):
+        if not np.isfinite(x[r, t[r]]):
+            x[r, t[r]] = 0.5
+    if dtype == "bf16":
+        xb = orc.f32_to_bf16_bits(x).reshape(x.shape)
+        x = orc.bf16_bits_to_f32(xb).reshape(x.shape)
+        xin, xt = xb, torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).cuda()
+    else:
+        xin, xt = x, torch.from_numpy(x).cuda()
+    T = x.shape[0]
+    w = np.full(T, 1.0 / T, np.float32)
+    a = np.linspace(-1, 1, T).astype(np.float32)
+    tm.set_force_generic(generic)
+    try:
+        met, dl, logp, ent = tm.pg_loss_fwd_bwd(xt, i32(t), f32(prob["old"]), f32(prob["ref"]), f32(a), f32(w),
+                                                want_logp=True)
+        lp2, ent2, _ = tm.logprob_fwd(xt, i32(t))
+        torch.cuda.synchronize()
+    finally:
+        tm.set_force_generic(False)
+    om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(xin, t, prob["old"], prob["ref"], a, w)
+    assert_close(logp.cpu().numpy(), olp, what="fused logp")
+    assert_close(ent.cpu().numpy(), oent, what="fused entropy")
+    assert_close(lp2.cpu().numpy(), olp, what="forward logp")
+    assert_close(ent2.cpu().numpy(), oent, what="forward entropy")
+    g = grad_to_np(dl)
+    assert np.isfinite(g).all()
+    near = near_clip_rows(olp, prob["old"], a, 0.2, 0.28)
+    assert_grad_close(g, odl, np.abs(og), dtype, rows_ok=~near)
+
+
 def test_pg_loss_all_masked_and_empty(tm, orc):
     from paper_2604_11554_b200 import _lib
 
