@@ -75,7 +75,10 @@ constexpr int kSlotCols = kCB / (128 * 4);  // TMEM columns per chunk slot (24)
 constexpr int kTSlots = 512 / kSlotCols;    // 21 TMEM chunk slots (252 KB)
 constexpr int kStore = kTSlots + kSSlots;   // row-store slots: TMEM first, then smem (31)
 constexpr int kTCols = 512;
-constexpr int kRD = 4;                      // depth of the per-row partial / scalar rings (flow-controlled)
+#ifndef SFTM_RD
+#define SFTM_RD 4
+#endif
+constexpr int kRD = SFTM_RD;                      // depth of the per-row partial / scalar rings (flow-controlled)
 // Mailbox ring depth (rows). Not flow-controlled across the cluster: with the
 // red/scal rings bounded, a CTA's control warp is at most 2*kRD+1 rows ahead
 // of its partner's mailbox reads, so 16 can never be overrun.
