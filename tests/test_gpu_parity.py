@@ -259,11 +259,13 @@ def test_pg_loss_unaligned_rows_use_fused_kernel(tm, orc):
     view.copy_(to_dev_logits(prob))
     cu, sid, mask, adv, adv_tok, w_tok = gpu_pipeline(tm, prob, 0)
     params = _lib.default_loss_params()
-    dl = torch.zeros_like(base)[:, 3:3 + V]
+    dbase = torch.full_like(base, 7.0)  # guard columns around every dlogits row
+    dl = dbase[:, 3:3 + V]
     met, dl, logp, ent = tm.pg_loss_fwd_bwd(view, i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]),
                                             adv_tok, w_tok, params, dlogits=dl, want_logp=True)
     torch.cuda.synchronize()
     assert tm.handle().last_launch()["kernel"] == "loss_tmem_kernel"
+    assert torch.all(dbase[:, :3] == 7.0) and torch.all(dbase[:, 3 + V:] == 7.0), "dlogits written out of row bounds"
     om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"],
                                                  adv_tok.cpu().numpy(), w_tok.cpu().numpy(), orc.params())
     act = w_tok.cpu().numpy() != 0
