@@ -8,7 +8,8 @@ from paper_2604_11554_b200 import train_math as tm
 dev = torch.device("cuda", 0)
 g = torch.Generator(device="cpu").manual_seed(1)
 SHAPES = [(torch.float32, 5000, 16000), (torch.bfloat16, 20000, 151936), (torch.float32, 20000, 4096),
-          (torch.bfloat16, 8000, 75968)]
+          (torch.bfloat16, 8000, 75968), (torch.bfloat16, 16000, 50257), (torch.bfloat16, 6000, 262144),
+          (torch.float32, 6000, 32001)]
 if os.environ.get("SHAPES"):
     SHAPES = [SHAPES[int(i)] for i in os.environ["SHAPES"].split(",")]
 for (dt, T, V) in SHAPES:
