@@ -344,7 +344,8 @@ std::mutex g_mu;
 template <typename T, int MODE, bool UA>
 int launch(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   auto kern = fwd_stream_kernel<T, MODE, UA>;
-  static int sms = -1;
+  static PerDevice cache;  // per instantiation and device
+  int& sms = cache();
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (sms < 0) {

@@ -74,6 +74,20 @@ __host__ __device__ inline size_t xp_index(unsigned long long epoch, int cta, in
   return ((static_cast<size_t>(epoch & 1) * kXpMaxCtas + cta) * kXpMailD + slot) * kXpMaxP + src;
 }
 
+// One-time launch setup (cudaFuncSetAttribute, occupancy queries) is per
+// device: a process may drive several GPUs. Indexed by the current device.
+struct PerDevice {
+  int v[64];
+  PerDevice() {
+    for (int& x : v) x = -1;
+  }
+  int& operator()() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return v[d & 63];
+  }
+};
+
 struct LaunchInfo {
   int kernel = 0;  // 0 = ring (TMA) kernel, 1 = generic two-pass kernel
   int cluster = 1;

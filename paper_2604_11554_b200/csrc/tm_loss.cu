@@ -1136,7 +1136,8 @@ std::mutex g_mu;
 template <typename T, int C, bool XP = false, bool UA = false>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
   auto kern = loss_tmem_kernel<T, C, XP, UA>;
-  static int max_active = -1;
+  static PerDevice cache;  // per instantiation and device
+  int& max_active = cache();
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (max_active < 0) {

@@ -564,7 +564,8 @@ std::mutex g_mu;
 template <typename T, int C>
 int launch_c(const RowArgs& a, int64_t slice, int lag, cudaStream_t s, LaunchInfo* info) {
   auto kern = loss_v3_kernel<T, C>;
-  static int max_active = -1;
+  static PerDevice cache;  // per instantiation and device
+  int& max_active = cache();
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (max_active < 0) {

@@ -460,7 +460,8 @@ template <typename T, int C, int MODE, int MINB>
 int launch_ring(const RowArgs& a, int64_t slice_elems, int nslots, int ring_bytes,
                 cudaStream_t s, LaunchInfo* info) {
   auto kern = rows_ring_kernel<T, C, MODE, MINB>;
-  static int max_active = -1;  // per instantiation
+  static PerDevice cache;  // per instantiation and device
+  int& max_active = cache();
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (max_active < 0) {

@@ -121,3 +121,31 @@ def test_vocab_parallel_nccl_matches_single_gpu():
     for r in res:
         if not all(r[1:-1]):
             pytest.fail("rank result: " + repr(r))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_one_process_two_devices():
+    """One process driving two GPUs: per-device launch setup (shared-memory
+    opt-in, occupancy) must hold on the second device too; same inputs give
+    bitwise the same outputs on both."""
+    from paper_2604_11554_b200 import train_math as tm
+
+    T, V = 300, 151936
+    g = torch.Generator(device="cpu").manual_seed(5)
+    x = (torch.randn(T, V, generator=g) * 2).to(torch.bfloat16)
+    y = torch.randint(0, V, (T,), generator=g, dtype=torch.int32)
+    old = torch.randn(T, generator=g) - 3
+    ref = old + 0.1 * torch.randn(T, generator=g)
+    adv = torch.randn(T, generator=g)
+    w = torch.full((T,), 1.0 / T)
+    outs = []
+    for d in (0, 1):
+        dev = torch.device("cuda", d)
+        with torch.cuda.device(dev):
+            met, dl, lp, ent = tm.pg_loss_fwd_bwd(x.to(dev), y.to(dev), old.to(dev), ref.to(dev), adv.to(dev),
+                                                  w.to(dev), want_logp=True)
+            lp2, _, _ = tm.logprob_fwd(x.to(dev), y.to(dev))
+            torch.cuda.synchronize(dev)
+            outs.append([t.cpu() for t in (met, dl, lp, ent, lp2)])
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
