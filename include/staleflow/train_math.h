@@ -31,7 +31,9 @@
  *     (a cudaStream_t passed as void*; NULL = legacy default stream).
  *   - handles are thread-compatible: one handle per role thread, or external
  *     synchronisation (the reference runs one thread per role,
- *     wall_runtime.cpp:296-315).
+ *     wall_runtime.cpp:296-315). The handle's scratch (metric partials,
+ *     host-call staging) is shared by its calls, so calls on one handle must
+ *     be ordered: one stream per handle, or a handle per concurrent stream.
  *
  * The math (decisions P1-P9 of SURVEY.md §8) is pinned in DESIGN.md §2 and
  * restated in fp64 by oracle/sf_oracle.c.
