@@ -221,17 +221,22 @@ def pg_step_host(logits, h_targets, h_old, h_ref, h_seq_lens, h_rewards, h_group
 
 
 # ---------------------------------------------------------------------- a5
-def r3_gate_fwd(router_logits, rec_idx, renorm: bool = True, want_idx: bool = True, want_mismatch: bool = True):
-    """router_logits [L, T, E] (f32/bf16), rec_idx [L, T, k] (int32/uint8)."""
+def r3_gate_fwd(router_logits, rec_idx, renorm: bool = True, want_idx: bool = True, want_mismatch: bool = True,
+                out=None):
+    """router_logits [L, T, E] (f32/bf16), rec_idx [L, T, k] (int32/uint8).
+    out: optional preallocated (w, idx, mismatch) to reuse."""
     d = _dev(router_logits)
     h = handle(d)
     L, T, E = router_logits.shape
     k = rec_idx.shape[-1]
     dt = _DT[router_logits.dtype]
     it = _lib.IDX_U8 if rec_idx.dtype == torch.uint8 else _lib.IDX_I32
-    w = torch.empty(L, T, k, dtype=torch.float32, device=router_logits.device)
-    idx = torch.empty(L, T, k, dtype=torch.int32, device=router_logits.device) if want_idx else None
-    mm = torch.empty(L + 1, dtype=torch.int32, device=router_logits.device) if want_mismatch else None
+    if out is not None:
+        w, idx, mm = out
+    else:
+        w = torch.empty(L, T, k, dtype=torch.float32, device=router_logits.device)
+        idx = torch.empty(L, T, k, dtype=torch.int32, device=router_logits.device) if want_idx else None
+        mm = torch.empty(L + 1, dtype=torch.int32, device=router_logits.device) if want_mismatch else None
     rc = _lib.lib().sf_tm_r3_gate_fwd(h.ptr, _p(router_logits.contiguous()), dt, L, T, E, k,
                                       _p(rec_idx.contiguous()), it, 1 if renorm else 0, _p(w), _p(idx), _p(mm),
                                       _stream(d))
@@ -239,14 +244,14 @@ def r3_gate_fwd(router_logits, rec_idx, renorm: bool = True, want_idx: bool = Tr
     return w, idx, mm
 
 
-def r3_gate_bwd(router_logits, rec_idx, w, dw, renorm: bool = True):
+def r3_gate_bwd(router_logits, rec_idx, w, dw, renorm: bool = True, out=None):
     d = _dev(router_logits)
     h = handle(d)
     L, T, E = router_logits.shape
     k = rec_idx.shape[-1]
     dt = _DT[router_logits.dtype]
     it = _lib.IDX_U8 if rec_idx.dtype == torch.uint8 else _lib.IDX_I32
-    dz = torch.empty_like(router_logits)
+    dz = torch.empty_like(router_logits) if out is None else out
     rc = _lib.lib().sf_tm_r3_gate_bwd(h.ptr, _p(router_logits), dt, L, T, E, k, _p(rec_idx), it,
                                       1 if renorm else 0, _p(w), _p(dw), _p(dz), _stream(d))
     h.check(rc, "sf_tm_r3_gate_bwd")
