@@ -966,13 +966,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float x[NE], gr[NE];
         unpack(logits, w0, w1, x);
+        // partial chunk: skip the math of vectors wholly outside the row (their
+        // stores are skipped too); `dep` ties a thread that stores nothing to
+        // its loads and scalars for the release ordering (dummy smem store)
+        bool vok0 = true, vok1 = true;
+        if (partial) {
+          const int lo = (UA && k == 0) ? mis : 0;
+          vok0 = (EV * btid + EV > lo) && (EV * btid < rem);
+          vok1 = (G::HALF + EV * btid + EV > lo) && (G::HALF + EV * btid < rem);
+        }
+        const uint32_t dep = w0.x ^ w1.w ^ __float_as_uint(lse2f) ^ rsc.sgn;
         if (mode == 0) {
           const float2 c2 = make_float2(c, c), nl2 = make_float2(-lse2f, -lse2f);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
-            const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
-            gr[2 * p] = ex2(av.x);
-            gr[2 * p + 1] = ex2(av.y);
+            if ((2 * p < EV) ? vok0 : vok1) {
+              const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+              gr[2 * p] = ex2(av.x);
+              gr[2 * p + 1] = ex2(av.y);
+            } else {
+              gr[2 * p] = gr[2 * p + 1] = 0.f;
+            }
           }
           if (k == ck) {
 #pragma unroll
@@ -1003,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (s1) stg128_cs(dst + G::HALF + EV * btid, p1);
             // a thread storing nothing still orders its loads before the
             // releases below through a dependent (dummy) smem store
-            if (!s0) sink_u32(sink_a, p0.x ^ p1.y);
+            if (!s0) sink_u32(sink_a, p0.x ^ p1.y ^ dep);
           }
           if (late) mbar_arrive(rel);
           return;
@@ -1012,10 +1026,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 mc0 = make_float2(-c0, -c0);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
-            const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
-            const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), mc0);
-            gr[2 * p] = g2.x;
-            gr[2 * p + 1] = g2.y;
+            if ((2 * p < EV) ? vok0 : vok1) {
+              const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+              const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), mc0);
+              gr[2 * p] = g2.x;
+              gr[2 * p + 1] = g2.y;
+            } else {
+              gr[2 * p] = gr[2 * p + 1] = 0.f;
+            }
           }
           if (k == ck) {
 #pragma unroll
@@ -1028,13 +1046,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 mc1 = make_float2(-c1, -c1), mc0 = make_float2(-c0, -c0);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
-            float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
-            av.x = fmaxf(av.x, -127.f);
-            av.y = fmaxf(av.y, -127.f);
-            const float2 t2 = __ffma2_rn(mc1, av, mc0);
-            const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), t2);
-            gr[2 * p] = g2.x;
-            gr[2 * p + 1] = g2.y;
+            if ((2 * p < EV) ? vok0 : vok1) {
+              float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
+              av.x = fmaxf(av.x, -127.f);
+              av.y = fmaxf(av.y, -127.f);
+              const float2 t2 = __ffma2_rn(mc1, av, mc0);
+              const float2 g2 = __fmul2_rn(make_float2(ex2(av.x), ex2(av.y)), t2);
+              gr[2 * p] = g2.x;
+              gr[2 * p + 1] = g2.y;
+            } else {
+              gr[2 * p] = gr[2 * p + 1] = 0.f;
+            }
           }
           if (k == ck) {
 #pragma unroll
@@ -1066,12 +1088,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
           }
-          if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]));
+          if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
         } else {
           const bool s0 = EV * btid < rem;
           if (s0) store_vec(dst + EV * btid, gr);
           if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
-          if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]));
+          if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
         }
         if (late) mbar_arrive(rel);
       };
