@@ -94,9 +94,9 @@ static_assert(2 * kXpCredit <= kMailD && kXpCredit < kCredD, "credit bounds");
 // Per-row scalars computed once by the control warp and broadcast in smem.
 struct RowScal {
   float lse2, lse2f, c0, c1, gt;
-  int yl;          // target column relative to this CTA's slice (or out of range)
+  int tck;         // chunk holding the target column in this CTA's slice, or -1
   uint32_t sgn;    // 0x80008000 when dlogits entries are -p*|c0| (bf16 fast path)
-  float pad;
+  uint32_t town;   // (thread owning the target << 8) | its element index j
 };
 constexpr int kMaxChunks = kStore - 2;      // a whole row slice must fit the row store
 
@@ -310,6 +310,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       (void)t;
       return 0;
+    }
+  };
+  // where the backward finds the target column (computed once per row by the
+  // control warp): chunk, owning thread and its element index
+  auto target_slot = [&](int64_t yl64, int mis, int& tck, uint32_t& town) {
+    tck = -1;
+    town = 0;
+    if (yl64 >= 0 && yl64 < slice_len) {
+      const int yp = static_cast<int>(yl64) + mis;  // sector coordinates
+      const int r = yp % CE;
+      const int v = r >= G::HALF ? 1 : 0;
+      const int rr = r - v * G::HALF;
+      tck = yp / CE;
+      town = (static_cast<uint32_t>(rr / EV) << 8) | static_cast<uint32_t>(v * EV + rr % EV);
     }
   };
 
@@ -730,8 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             r.c1 = a.inv_tau * gH * kLn2;
             r.lse2f = lse2 - log2f(fabsf(r.c0));
             r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
-            r.yl = (yl64 >= 0 && yl64 < slice_len) ? static_cast<int>(yl64) : -1;
-            r.pad = 0.f;
+            target_slot(yl64, row_mis(t), r.tck, r.town);
             mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
             scal[rs] = r;
             mbar_arrive(smem_u32(&scal_bar[rs]));
@@ -837,8 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         r.c1 = a.inv_tau * gH * kLn2;
         r.lse2f = lse2 - log2f(fabsf(r.c0));
         r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
-        r.yl = (yl64 >= 0 && yl64 < slice_len) ? static_cast<int>(yl64) : -1;
-        r.pad = 0.f;
+        target_slot(yl64, row_mis(t), r.tck, r.town);
 #ifndef SFTM_NO_FLOWCTL
         mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
 #endif
@@ -909,17 +921,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const RowScal rsc = scal[rs];
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
-      int ck = -1, jt = 0;
-      if (rsc.yl >= 0) {
-        const int yp = rsc.yl + mis;  // sector coordinates
-        const int r = yp % CE;
-        const int v = r >= G::HALF ? 1 : 0;
-        const int rr = r - v * G::HALF;
-        if (rr / EV == btid) {
-          ck = yp / CE;
-          jt = v * EV + rr % EV;
-        }
-      }
+      const int ck = (static_cast<int>(rsc.town >> 8) == btid) ? rsc.tck : -1;
+      const int jt = static_cast<int>(rsc.town & 0xffu);
       // dlogits rows share the logits rows' sector phase (checked at dispatch)
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start - mis;
       const uint32_t sgn = neg ? 0x80008000u : 0u;
@@ -1131,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // the row's stores consumed every lane's scalars (a row with no chunk
       // here consumes them through a dependent dummy smem store): free the slot
-      if (nck_r == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.yl);
+      if (nck_r == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.town);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;

@@ -6,7 +6,7 @@ from paper_2604_11554_b200 import train_math as tm
 
 dev = torch.device("cuda", 0)
 T = 131072
-for V in [18432, 24576, 30720, 36864, 37984, 43008, 49152, 75968]:
+for V in [int(v) for v in os.environ.get('VS', '18432,24576,30720,36864,37984,43008,49152,75968').split(',')]:
     lg = torch.empty(T, V, dtype=torch.bfloat16, device=dev)
     tm.synth_logits(lg, seed=3, sigma=2.0)
     g = torch.Generator(device=dev).manual_seed(1)
