@@ -5,9 +5,9 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 reference legs may import this module, and only as the checker or as the timed
 CPU baseline. It never backs a product call.
 
-Parity status (see sf_oracle.h and DESIGN.md §3): the reference has no code for
-this math, so the oracle restates the published algorithms with the P1-P9
-decisions; it is pinned by hand-derived known answers and by golden vectors
+Parity status (see sf_oracle.h and DESIGN.md §3): math parity unpinned against
+the reference — the reference has no code for this math, so the oracle
+restates the published algorithms with the P1-P9 decisions; it is pinned by hand-derived known answers and by golden vectors
 from an independent torch-float64 autograd implementation
 (tests/golden/make_golden.py). The seeded RNG and digest helpers are pinned
 bit-exactly against the reference's own rng.cpp / hash.hpp (oracle/_ref).

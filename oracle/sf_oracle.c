@@ -9,6 +9,14 @@
  * decoupled clip, loss only over assistant tokens
  * (PAPER.md:332), cu_seqlens packing, R3 replay
  * (PAPER.md:563-565), with the P1-P9 decisions of DESIGN.md §2.
+ *
+ * Parity status: math parity unpinned against the reference, because the
+ * reference has no implementation, test, fixture or golden vector for it
+ * (SURVEY.md §8c). The restatement is pinned instead by hand-derived known
+ * answers and by golden vectors from an independent torch-float64 autograd
+ * implementation (tests/golden/make_golden.py); its seeded RNG and digest
+ * helpers are pinned bit-exactly against the reference's own rng.cpp /
+ * hash.hpp compiled in oracle/_ref.
  */
 #include "sf_oracle.h"
 
