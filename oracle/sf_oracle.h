@@ -6,7 +6,8 @@
  * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
  * may load it, and only as the checker or the timed CPU baseline.
  *
- * Parity status: the reference (/root/reference) contains NO implementation of
+ * Parity status: math parity unpinned against the reference. The reference
+ * (/root/reference) contains NO implementation of
  * this math (SPEC.md:8 puts GRPO/DAPO losses and R3 internals out of scope;
  * the compute is a latency stub at proj/src/sim_runtime.cpp:441 and
  * proj/src/wall_runtime.cpp:118,174,197). The oracle is therefore a
