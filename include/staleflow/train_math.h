@@ -266,7 +266,8 @@ int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, in
  * Then every rank calls sf_tm_vp_fused_loss_fwd_bwd with the same T, w_tok and
  * call sequence (calls are matched by order). Outputs are as
  * sf_tm_vp_loss_fwd_bwd; metrics, logp and entropy are identical on all ranks.
- * A rank whose peers never launch traps after 20 s (no silent hang). */
+ * A rank whose peers never launch traps after SF_TM_XP_TIMEOUT_S seconds
+ * (environment, default 300) instead of hanging silently. */
 #define SF_TM_IPC_HANDLE_BYTES 64
 int sf_tm_vp_mailbox_create(sf_tm_t h, int32_t P, int32_t rank, void* ipc_handle_out);
 int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles);

@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -743,6 +744,12 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
   a.xp_rank = h->xp_rank;
   a.xp_epoch = h->xp_epoch;
   a.xp_err = h->xp_err;
+  static const unsigned long long timeout_ns = [] {
+    const char* v = getenv("SF_TM_XP_TIMEOUT_S");
+    const double sec = v ? atof(v) : 300.0;
+    return static_cast<unsigned long long>((sec > 0 ? sec : 300.0) * 1e9);
+  }();
+  a.xp_timeout_ns = timeout_ns;
   a.partials = h->partials;
   a.ticket = h->ticket;
   a.max_partial_blocks = h->max_partial_blocks;

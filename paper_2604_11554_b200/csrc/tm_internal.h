@@ -47,6 +47,7 @@ struct RowArgs {
   int xp_rank = 0, xp_P = 0;
   unsigned long long xp_epoch = 0;  // launch sequence number, identical on all ranks
   int* xp_err = nullptr;            // set to 1 before trapping on an exchange timeout
+  unsigned long long xp_timeout_ns = 300000000000ull;  // SF_TM_XP_TIMEOUT_S (default 300 s)
   // optional wait-time instrumentation (debug only): per-role clock64 sums
   unsigned long long* dbg = nullptr;
   // workspace (owned by the handle)

@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t t0 = globaltimer_ns();
               do {
                 __nanosleep(64);
-                if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a peer never launched
+                if (globaltimer_ns() - t0 > a.xp_timeout_ns) {  // a peer never launched
                   if (a.xp_err) atomicExch(a.xp_err, 1);
                   __trap();
                 }
