@@ -565,6 +565,22 @@ def test_cluster_size_parity(C):
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
+def test_fwd_ring_baseline_parity():
+    """The older 16-warp ring kernel, kept as the A/B baseline of the forward
+    modes (SFTM_FWD_RING=1), still meets the parity bar."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFTM_FWD_RING="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
+                          "(test_logprob_fwd and not odd_stride) or vocab_parallel_matches_fused",
+                          "--timeout", "120"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 def test_v3_schedule_parity():
     """The per-warp software-pipelined schedule (tm_loss3.cu, SFTM_LOSS_VARIANT=3)
     must meet the same parity bar as the default schedule."""
