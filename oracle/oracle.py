@@ -58,6 +58,8 @@ def lib():
             "orc_token_weights": (_i32, [_vp, _i64, _vp, _vp, _i64, _i32, _d, _vp, _vp]),
             "orc_pg_loss_fwd_bwd": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                            ctypes.POINTER(OrcParams), _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
+            "orc_pg_loss_fwd_bwd_fast": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                                                ctypes.POINTER(OrcParams), _vp, _vp]),
             "orc_r3_gate_fwd": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _i32, _vp, _vp, _vp]),
             "orc_r3_gate_bwd": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _i32, _vp, _vp, _vp]),
             "orc_vp_partial_stats": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _d, _vp]),
@@ -204,6 +206,21 @@ def pg_loss_fwd_bwd(logits, targets, old, ref, adv_tok, w_tok, p: OrcParams = No
     lib().orc_pg_loss_fwd_bwd(_ptr(logits), _dtype_code(logits), T, V, V, *[_ptr(a) for a in args], ctypes.byref(p),
                               1 if masked_skip else 0, _ptr(dl), dl_dtype, _ptr(logp), _ptr(ent), _ptr(met), _ptr(g))
     return met, dl, logp, ent, g
+
+
+def pg_loss_fwd_bwd_fast(logits_bits, targets, old, ref, adv_tok, w_tok, p: OrcParams = None):
+    """The timed CPU baseline (sf_cpu_fast.c): bf16 bits in, bf16 bits out, fp32
+    arithmetic. Returns (metrics, dlogits_bits)."""
+    if p is None:
+        p = params()
+    x = np.ascontiguousarray(logits_bits, dtype=np.uint16)
+    T, V = x.shape
+    args = [np.ascontiguousarray(a, dtype=dt) for a, dt in
+            ((targets, np.int32), (old, np.float32), (ref, np.float32), (adv_tok, np.float32), (w_tok, np.float32))]
+    dl = np.empty((T, V), np.uint16)
+    met = np.empty(8)
+    lib().orc_pg_loss_fwd_bwd_fast(_ptr(x), T, V, V, *[_ptr(a) for a in args], ctypes.byref(p), _ptr(dl), _ptr(met))
+    return met, dl
 
 
 def r3_gate_fwd(logits, rec, renorm=True):

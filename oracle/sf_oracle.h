@@ -63,6 +63,13 @@ int orc_pg_loss_fwd_bwd(const void* logits, int dtype, int64_t T, int64_t V, int
                         int masked_skip, void* dlogits, int dl_dtype, double* logp, double* ent,
                         double* metrics, double* g_out);
 
+/* The timed CPU baseline ("fast" variant, sf_cpu_fast.c): bf16 logits -> bf16
+ * dlogits [T, V], fp32 arithmetic, vectorised, OpenMP over rows; finite logits.
+ * Same math as orc_pg_loss_fwd_bwd; checked against it in tests/test_oracle.py. */
+int orc_pg_loss_fwd_bwd_fast(const uint16_t* logits, int64_t T, int64_t V, int64_t ld, const int32_t* targets,
+                             const float* old_logp, const float* ref_logp, const float* adv_tok,
+                             const float* w_tok, const orc_params* p, uint16_t* dlogits, double* metrics);
+
 /* a5 */
 int orc_r3_gate_fwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E, int64_t k,
                     const void* rec, int idx_dtype, int renorm, double* w, int32_t* idx,

@@ -213,3 +213,21 @@ def test_vp_partial_stats_combine_equals_full_row(orc):
     assert np.allclose(L, lse, atol=1e-12)
     assert np.allclose(np.log(S) - W / S, ent, atol=1e-12)
     assert np.allclose(zy - L, logp, atol=1e-12)
+
+
+def test_fast_cpu_baseline_matches_fp64_oracle(orc):
+    """The fp32 'fast' CPU variant timed as the CPU baseline computes the same
+    loss: metrics within fp32 tolerance, dlogits within 2 bf16 ulp."""
+    prob = orc.synth_problem(13, [20, 17], 5000, "bf16", prompt_max=4)
+    T = prob["T"]
+    rng = np.random.default_rng(2)
+    a = rng.normal(size=T).astype(np.float32)
+    w = (rng.random(T) < 0.8).astype(np.float32) / T
+    p = orc.params(beta=0.05, ent_coef=0.01)
+    om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, p)
+    fm, fdl = orc.pg_loss_fwd_bwd_fast(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, p)
+    assert np.allclose(fm[:6], om[:6], rtol=1e-4, atol=1e-6) and fm[6] == om[6]
+    g = orc.bf16_bits_to_f32(fdl.ravel()).reshape(fdl.shape).astype(np.float64)
+    ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(odl), 1e-38))) - 7)
+    err = np.abs(g - odl) - 2 * ulp - 1e-6 * np.abs(og)[:, None]
+    assert (err <= 0).mean() > 0.999
