@@ -186,7 +186,12 @@ int sf_tm_token_weights(sf_tm_t h, const int32_t* cu_seqlens, int64_t B, const f
  * row stride ld_d; dlogits == logits (in place) is supported. out_metrics is
  * device float[SF_TM_NUM_METRICS] (deterministic fixed-order reduction).
  * out_logp / out_entropy optional. Replaces the trainer seam latency
- * (sim_runtime.cpp:441, wall_runtime.cpp:197). */
+ * (sim_runtime.cpp:441, wall_runtime.cpp:197).
+ * Kernel choice (transparent): any element-aligned rows take the single-pass
+ * kernel when dlogits rows sit at the same 16-byte phase as the logits rows
+ * (same base alignment mod 16, stride difference a multiple of 16 bytes) and
+ * a row slice fits the row store; otherwise a two-pass kernel computes the
+ * same outputs. sf_tm_last_launch reports which ran. */
 int sf_tm_pg_loss_fwd_bwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
                           int64_t ld, const int32_t* targets, const float* old_logp,
                           const float* ref_logp, const float* adv_tok, const float* w_tok,
