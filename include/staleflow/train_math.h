@@ -102,8 +102,15 @@ typedef struct sf_tm_loss_params {
   int32_t norm_mode;     /* SF_TM_NORM_*                              */
   float inv_norm;        /* used when norm_mode == SF_TM_NORM_EXPLICIT */
   int32_t masked_rows;   /* SF_TM_MASKED_*                            */
-  int32_t reserved;
+  int32_t kl_mode;       /* P5: SF_TM_KL_* estimator (0 = k3, default) */
 } sf_tm_loss_params;
+
+/* KL estimators, d = ref_logp - logp (veRL's kl_loss_type names in brackets):
+ * K3 e^d - d - 1 [low_var_kl], K1 -d [kl], K2 d^2/2 [mse], ABS |d| [abs]. */
+#define SF_TM_KL_K3 0
+#define SF_TM_KL_K1 1
+#define SF_TM_KL_K2 2
+#define SF_TM_KL_ABS 3
 
 /* Fills the DAPO defaults above (eps 0.2/0.28, no dual clip, beta 0,
  * ent 0, tau 1, token-mean, zero-fill). */

@@ -32,7 +32,8 @@ _u64 = ctypes.c_uint64
 
 
 class OrcParams(ctypes.Structure):
-    _fields_ = [("eps_lo", _d), ("eps_hi", _d), ("dual_c", _d), ("beta", _d), ("ent_coef", _d), ("inv_tau", _d)]
+    _fields_ = [("eps_lo", _d), ("eps_hi", _d), ("dual_c", _d), ("beta", _d), ("ent_coef", _d), ("inv_tau", _d),
+                ("kl_mode", ctypes.c_int32)]
 
 
 _lib = None
@@ -183,8 +184,8 @@ def token_weights(cu, adv_seq, mask, T, norm_mode=0, inv_norm=0.0):
     return adv_tok, w_tok
 
 
-def params(eps_lo=0.2, eps_hi=0.28, dual_c=0.0, beta=0.0, ent_coef=0.0, inv_tau=1.0) -> OrcParams:
-    return OrcParams(eps_lo, eps_hi, dual_c, beta, ent_coef, inv_tau)
+def params(eps_lo=0.2, eps_hi=0.28, dual_c=0.0, beta=0.0, ent_coef=0.0, inv_tau=1.0, kl_mode=0) -> OrcParams:
+    return OrcParams(eps_lo, eps_hi, dual_c, beta, ent_coef, inv_tau, kl_mode)
 
 
 def pg_loss_fwd_bwd(logits, targets, old, ref, adv_tok, w_tok, p: OrcParams = None, masked_skip=False,

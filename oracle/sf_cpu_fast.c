@@ -106,8 +106,23 @@ int orc_pg_loss_fwd_bwd_fast(const uint16_t* logits, int64_t T, int64_t V, int64
       }
     }
     const int has_kl = p->beta != 0.0;
-    const float d = ref - lp, er = expf(d), kl = er - d - 1.f;
-    const float g = w * (gpg + (has_kl ? (float)p->beta * (1.f - er) : 0.f));
+    const float d = ref - lp;
+    float kl, dkl;
+    if (p->kl_mode == 1) {
+      kl = -d;
+      dkl = 1.f;
+    } else if (p->kl_mode == 2) {
+      kl = 0.5f * d * d;
+      dkl = -d;
+    } else if (p->kl_mode == 3) {
+      kl = fabsf(d);
+      dkl = d > 0.f ? -1.f : (d < 0.f ? 1.f : 0.f);
+    } else {
+      const float er = expf(d);
+      kl = er - d - 1.f;
+      dkl = 1.f - er;
+    }
+    const float g = w * (gpg + (has_kl ? (float)p->beta * dkl : 0.f));
     const float gH = -w * (float)p->ent_coef;
     double* mr = rowm + t * 8;
     mr[0] = w * (pg + (has_kl ? (float)p->beta * kl : 0.f) - (float)p->ent_coef * H);

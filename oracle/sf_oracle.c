@@ -274,11 +274,27 @@ int orc_pg_loss_fwd_bwd(const void* logits, int dtype, int64_t T, int64_t V, int
         clipped = 1;
       }
     }
+    /* KL estimators (d = ref - logp) and their derivative in logp: k3 e^d-d-1
+     * (1-e^d), k1 -d (1), k2 d^2/2 (-d), abs |d| (-sign d); beta = 0 drops them */
     const double d = ref - lp;
-    const double er = exp(d);
-    const double kl = er - d - 1.0;
-    const double gkl = p->beta * (1.0 - er);
-    const double l = pg + p->beta * kl - p->ent_coef * H;
+    double kl, dkl;
+    if (p->kl_mode == 1) {
+      kl = -d;
+      dkl = 1.0;
+    } else if (p->kl_mode == 2) {
+      kl = 0.5 * d * d;
+      dkl = -d;
+    } else if (p->kl_mode == 3) {
+      kl = fabs(d);
+      dkl = d > 0.0 ? -1.0 : (d < 0.0 ? 1.0 : 0.0);
+    } else {
+      const double er = exp(d);
+      kl = er - d - 1.0;
+      dkl = 1.0 - er;
+    }
+    const int has_kl = p->beta != 0.0;
+    const double gkl = has_kl ? p->beta * dkl : 0.0;
+    const double l = pg + (has_kl ? p->beta * kl : 0.0) - p->ent_coef * H;
     const double g = w * (gpg + gkl);
     const double gH = -w * p->ent_coef;
     mrow[0] = w * l;

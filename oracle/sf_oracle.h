@@ -29,6 +29,7 @@ extern "C" {
 
 typedef struct orc_params {
   double eps_lo, eps_hi, dual_c, beta, ent_coef, inv_tau;
+  int32_t kl_mode; /* 0 k3, 1 k1, 2 k2, 3 abs (SF_TM_KL_*) */
 } orc_params;
 
 /* dtype: 0 = f32, 1 = bf16 (raw uint16), 2 = f64 (oracle outputs only) */

@@ -51,11 +51,12 @@ class LossParams(ctypes.Structure):
         ("norm_mode", ctypes.c_int32),
         ("inv_norm", ctypes.c_float),
         ("masked_rows", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("kl_mode", ctypes.c_int32),
     ]
 
 
 IPC_HANDLE_BYTES = 64  # SF_TM_IPC_HANDLE_BYTES
+KL_K3, KL_K1, KL_K2, KL_ABS = 0, 1, 2, 3  # SF_TM_KL_*
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32

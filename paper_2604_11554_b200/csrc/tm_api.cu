@@ -126,6 +126,8 @@ int check_loss_params(sf_tm_t h, const sf_tm_loss_params* p) {
     return fail(h, SF_TM_CONFIG_ERROR, "inv_norm must be finite and >= 0");
   if (p->masked_rows != SF_TM_MASKED_ZERO_FILL && p->masked_rows != SF_TM_MASKED_SKIP)
     return fail(h, SF_TM_CONFIG_ERROR, "masked_rows must be SF_TM_MASKED_*");
+  if (p->kl_mode < SF_TM_KL_K3 || p->kl_mode > SF_TM_KL_ABS)
+    return fail(h, SF_TM_CONFIG_ERROR, "kl_mode must be SF_TM_KL_*");
   return SF_TM_OK;
 }
 
@@ -148,6 +150,7 @@ void fill_loss(sftm::RowArgs& a, const sf_tm_loss_params* p) {
   a.ent_coef = p->entropy_coef;
   a.inv_tau = p->inv_temperature;
   a.masked_skip = p->masked_rows == SF_TM_MASKED_SKIP ? 1 : 0;
+  a.kl_mode = p->kl_mode;
 }
 
 int run_rows(sf_tm_t h, sftm::RowArgs& a, int mode, cudaStream_t s, const char* where) {

@@ -31,6 +31,7 @@ struct RowArgs {
   const float* w_tok = nullptr;
   float eps_lo = 0.2f, eps_hi = 0.28f, dual_c = 0.f, beta = 0.f, ent_coef = 0.f;
   int masked_skip = 0;
+  int kl_mode = 0;  // SF_TM_KL_*
   void* dlogits = nullptr;
   int64_t ld_d = 0;
   // outputs

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kCtl) {
     // ================================================================ control
-    const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
+    const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef, a.kl_mode};
     const bool leader = (crank == 0 && lane == 0);
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t nrow = 0;

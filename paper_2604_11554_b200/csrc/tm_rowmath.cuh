@@ -86,6 +86,7 @@ __device__ __forceinline__ void accum8(Stats& st, const float x[8], float c) {
 
 struct LossParamsDev {
   float eps_lo, eps_hi, dual_c, beta, ent;
+  int kl_mode = 0;  // SF_TM_KL_*: 0 k3, 1 k1, 2 k2, 3 abs
 };
 
 // Per-row scalars from merged statistics. Decision P1: z = x / tau.
@@ -119,12 +120,27 @@ __device__ __forceinline__ void loss_terms(float logp, float H, float w, float A
     }
   }
   const float d = ref - logp;
-  const float er = expf(d);
-  const float kl = er - d - 1.f;
+  // KL estimator and its derivative in logp (d = ref - logp): k3 e^d - d - 1
+  // (1 - e^d), k1 -d (1), k2 d^2/2 (-d), abs |d| (-sign d)
+  float kl, dkl;
+  if (P.kl_mode == 1) {
+    kl = -d;
+    dkl = 1.f;
+  } else if (P.kl_mode == 2) {
+    kl = 0.5f * d * d;
+    dkl = -d;
+  } else if (P.kl_mode == 3) {
+    kl = fabsf(d);
+    dkl = d > 0.f ? -1.f : (d < 0.f ? 1.f : 0.f);
+  } else {
+    const float er = expf(d);
+    kl = er - d - 1.f;
+    dkl = 1.f - er;
+  }
   // beta == 0 must drop the KL terms entirely: e^(ref - logp) overflows fp32 for
   // rows the policy gives far less mass than the reference (0 * inf = NaN)
   const bool has_kl = P.beta != 0.f;
-  const float gkl = has_kl ? P.beta * (1.f - er) : 0.f;
+  const float gkl = has_kl ? P.beta * dkl : 0.f;
   const float l = pg + (has_kl ? P.beta * kl : 0.f) - P.ent * H;
   g = w * (gpg + gkl);
   gH = -w * P.ent;

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   } else {
     // ------------------------------------------------------------ consumers
     const float c = a.inv_tau * kLog2e;
-    const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
+    const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef, a.kl_mode};
     uint32_t slot = 0, ph = 0, nrow = 0;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const bool leader = (crank == 0 && tid == 0);
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kGT) rows_generic_kernel(const RowArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const T* logits = static_cast<const T*>(a.logits);
   const float c = a.inv_tau * kLog2e;
-  const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef};
+  const LossParamsDev P{a.eps_lo, a.eps_hi, a.dual_c, a.beta, a.ent_coef, a.kl_mode};
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   for (int64_t t = blockIdx.x; t < a.T; t += gridDim.x) {

@@ -55,3 +55,14 @@ def near_clip_rows(logp_ref, old, adv, eps_lo, eps_hi, dual_c=0.0, tol=1e-5):
     if dual_c > 1:
         near |= (a < 0) & (np.abs(r - dual_c) < tol * dual_c)
     return near
+
+
+def loss_row_scale(og, w, a, olp, old, ref, beta=0.0, kl_mode=0, ent=0.0, inv_tau=1.0):
+    """Per-row gradient magnitude before cancellation: |g| can be far smaller than
+    the policy and KL terms it is the sum of (fp32 error follows the terms)."""
+    w = np.abs(np.asarray(w, np.float64))
+    ratio = np.exp(np.asarray(olp, np.float64) - np.asarray(old, np.float64))
+    d = np.asarray(ref, np.float64) - np.asarray(olp, np.float64)
+    dkl = {0: np.abs(1 - np.exp(np.minimum(d, 80))), 1: np.ones_like(d), 2: np.abs(d), 3: np.ones_like(d)}[kl_mode]
+    terms = np.abs(np.asarray(a, np.float64)) * ratio + abs(beta) * dkl
+    return (np.abs(og) + w * terms + w * abs(ent) * 60.0) * inv_tau

@@ -6,7 +6,7 @@ tolerances (tests/_cmp.py) for floating point."""
 import numpy as np
 import pytest
 
-from tests._cmp import assert_close, assert_grad_close, near_clip_rows
+from tests._cmp import assert_close, assert_grad_close, loss_row_scale, near_clip_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -78,7 +78,7 @@ def check_loss_case(tm, orc, prob, pkw=None, generic=False, in_place=False, mask
     w = w_tok.cpu().numpy()
     a = adv_tok.cpu().numpy()
     op = orc.params(params.clip_eps_low, params.clip_eps_high, params.dual_clip_c, params.kl_beta,
-                    params.entropy_coef, params.inv_temperature)
+                    params.entropy_coef, params.inv_temperature, params.kl_mode)
     om, odl, olp, oent, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, op,
                                                  masked_skip=masked_skip)
     act = w != 0
@@ -89,7 +89,8 @@ def check_loss_case(tm, orc, prob, pkw=None, generic=False, in_place=False, mask
     gm = met.cpu().numpy()
     near = near_clip_rows(olp, prob["old"], a, params.clip_eps_low, params.clip_eps_high, params.dual_clip_c)
     near &= act
-    scale = (np.abs(og) + np.abs(w) * abs(params.entropy_coef) * 60.0) * params.inv_temperature
+    scale = loss_row_scale(og, w, a, olp, prob["old"], prob["ref"], params.kl_beta, params.kl_mode,
+                           params.entropy_coef, params.inv_temperature)
     gdl = grad_to_np(dl)
     if masked_skip:
         assert np.all(gdl[~act] == sentinel)
@@ -236,6 +237,9 @@ LOSS_CASES = [
     ("bf16_odd_vocab_skip", "bf16", 20011, [25, 25], {}, {"masked_skip": True}),
     ("bf16_odd_tiny", "bf16", 13, [9, 9], {}, {}),
     ("bf16_tiny_vocab", "bf16", 16, [9, 9], {"kl_beta": 0.1}, {}),
+    ("kl_k1_f32", "f32", 4096, [20, 11], {"kl_beta": 0.1, "kl_mode": 1}, {}),
+    ("kl_k2_bf16", "bf16", 32000, [17, 9], {"kl_beta": 0.1, "kl_mode": 2}, {}),
+    ("kl_abs_bf16_odd", "bf16", 20011, [13, 15], {"kl_beta": 0.1, "kl_mode": 3}, {}),
 ]
 
 

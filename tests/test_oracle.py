@@ -231,3 +231,23 @@ def test_fast_cpu_baseline_matches_fp64_oracle(orc):
     ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(odl), 1e-38))) - 7)
     err = np.abs(g - odl) - 2 * ulp - 1e-6 * np.abs(og)[:, None]
     assert (err <= 0).mean() > 0.999
+
+
+@pytest.mark.parametrize("kl_mode", [0, 1, 2, 3])
+def test_kl_estimators_known_answer(orc, kl_mode):
+    """The four KL estimators (d = ref - logp): k3 e^d - d - 1, k1 -d, k2 d^2/2,
+    abs |d|; metric 2 is sum w*kl and g_t = w*(g_pg + beta*dkl/dlogp)."""
+    prob = orc.synth_problem(17, [9, 8], 600, "f32", prompt_max=0)
+    T = prob["T"]
+    a = np.zeros(T, np.float32)  # no policy term: g is the KL gradient alone
+    w = np.full(T, 1.0 / T, np.float32)
+    beta = 0.3
+    om, _, olp, _, og = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w,
+                                            orc.params(beta=beta, kl_mode=kl_mode))
+    d = prob["ref"].astype(np.float64) - olp
+    kl, dkl = {0: (np.exp(d) - d - 1, 1 - np.exp(d)), 1: (-d, np.ones_like(d)), 2: (0.5 * d * d, -d),
+               3: (np.abs(d), -np.sign(d))}[kl_mode]
+    w64 = w.astype(np.float64)
+    assert np.isclose(om[2], (w64 * kl).sum(), rtol=1e-10, atol=1e-14)
+    assert np.isclose(om[0], beta * (w64 * kl).sum(), rtol=1e-10, atol=1e-14)
+    assert np.allclose(og, w64 * beta * dkl, rtol=1e-10, atol=1e-14)
