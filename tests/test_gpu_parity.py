@@ -395,6 +395,28 @@ def test_pg_loss_all_masked_and_empty(tm, orc):
     assert ex.value.code == _lib.CONFIG_ERROR
 
 
+def test_config_errors_are_reported(tm, orc):
+    """Bad arguments return ConfigError (21) with a message, never a launch."""
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(4, [5], 4096, "bf16")
+    x = to_dev_logits(prob)
+    t, o, r = i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"])
+    z = torch.zeros(5, device="cuda")
+    bad = [dict(kl_mode=7), dict(norm_mode=9), dict(masked_rows=5), dict(inv_temperature=-1.0),
+           dict(kl_beta=float("nan"))]
+    for kw in bad:
+        with pytest.raises(_lib.TrainMathError) as ex:
+            tm.pg_loss_fwd_bwd(x, t, o, r, z, z, _lib.default_loss_params(**kw))
+        assert ex.value.code == _lib.CONFIG_ERROR and str(ex.value), kw
+    with pytest.raises(_lib.TrainMathError) as ex:  # the fused vocab-parallel call needs open mailboxes
+        tm.vp_fused_loss_fwd_bwd(x, 0, t, o, r, z, z)
+    assert ex.value.code == _lib.CONFIG_ERROR
+    with pytest.raises(_lib.TrainMathError) as ex:  # no CPU path
+        tm.pg_loss_fwd_bwd(x.cpu(), t, o, r, z, z)
+    assert ex.value.code == _lib.CONFIG_ERROR
+
+
 def test_pg_step_host_matches_oracle_pipeline(tm, orc):
     from paper_2604_11554_b200 import _lib
 
