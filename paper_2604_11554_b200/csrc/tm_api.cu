@@ -54,6 +54,33 @@ struct sf_tm_handle {
   float* d_adv = nullptr;
   int32_t* d_total = nullptr;
   float* d_metrics = nullptr;
+  // sf_tm_pg_step_host pipeline: two prologue stages (bus-field H2D, varlen,
+  // GRPO, token weights) run on `side` while the caller's stream runs the
+  // previous micro-batch's fused loss; each stage is reused two calls later,
+  // after the loss that read it (free_ev).
+  struct HostStage {
+    int64_t tcap = 0, bcap = 0;
+    int32_t* targets = nullptr;
+    float* old = nullptr;
+    float* ref = nullptr;
+    uint8_t* mask = nullptr;
+    float* advtok = nullptr;
+    float* wtok = nullptr;
+    int32_t* lens = nullptr;
+    int32_t* plens = nullptr;
+    float* rewards = nullptr;
+    int32_t* gids = nullptr;
+    int32_t* cu = nullptr;
+    float* adv = nullptr;
+    int32_t* cnt = nullptr;
+    int32_t* total = nullptr;
+    unsigned* ticket = nullptr;
+    int64_t* tot = nullptr;
+    cudaEvent_t ready_ev = nullptr;
+    cudaEvent_t free_ev = nullptr;
+  } st[2];
+  int st_next = 0;
+  cudaStream_t side = nullptr;
 };
 
 namespace {
@@ -189,6 +216,59 @@ int ensure_bscratch(sf_tm_t h, int64_t B) {
   return SF_TM_OK;
 }
 
+// Stage buffers for sf_tm_pg_step_host (grow-once; the first use creates the
+// side stream, the events and the per-stage counters).
+int ensure_stage(sf_tm_t h, sf_tm_handle::HostStage& g, int64_t T, int64_t B) {
+  if (!h->side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(h, e, "pg_step_host side stream");
+  }
+  if (!g.ready_ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&g.ready_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g.free_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&g.ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&g.tot, sizeof(int64_t) * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&g.total, sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemset(g.ticket, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // the zeroed ticket before any side-stream use
+    if (e != cudaSuccess) return cuda_fail(h, e, "pg_step_host stage");
+  }
+  int rc = 0;
+  if (T > g.tcap) {
+    // a grow frees buffers a pending launch may still read
+    if (cudaError_t e = cudaEventSynchronize(g.free_ev)) return cuda_fail(h, e, "pg_step_host stage");
+    if ((rc = grow(h, &g.targets, T, "scratch")) || (rc = grow(h, &g.old, T, "scratch")) ||
+        (rc = grow(h, &g.ref, T, "scratch")) || (rc = grow(h, &g.mask, T, "scratch")) ||
+        (rc = grow(h, &g.advtok, T, "scratch")) || (rc = grow(h, &g.wtok, T, "scratch")))
+      return rc;
+    g.tcap = T;
+  }
+  if (B > g.bcap) {
+    if (cudaError_t e = cudaEventSynchronize(g.free_ev)) return cuda_fail(h, e, "pg_step_host stage");
+    const int64_t cap = B < 1024 ? 1024 : B;
+    if ((rc = grow(h, &g.lens, cap, "scratch")) || (rc = grow(h, &g.plens, cap, "scratch")) ||
+        (rc = grow(h, &g.rewards, cap, "scratch")) || (rc = grow(h, &g.gids, cap, "scratch")) ||
+        (rc = grow(h, &g.cu, cap + 1, "scratch")) || (rc = grow(h, &g.adv, cap, "scratch")) ||
+        (rc = grow(h, &g.cnt, cap, "scratch")))
+      return rc;
+    g.bcap = cap;
+  }
+  return SF_TM_OK;
+}
+
+void free_stages(sf_tm_t h) {
+  if (h->side) cudaStreamSynchronize(h->side);
+  for (auto& g : h->st) {
+    void* ptrs[] = {g.targets, g.old, g.ref, g.mask, g.advtok, g.wtok, g.lens, g.plens, g.rewards,
+                    g.gids, g.cu, g.adv, g.cnt, g.total, g.ticket, g.tot};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (g.ready_ev) cudaEventDestroy(g.ready_ev);
+    if (g.free_ev) cudaEventDestroy(g.free_ev);
+  }
+  if (h->side) cudaStreamDestroy(h->side);
+}
+
 }  // namespace
 
 extern "C" {
@@ -252,6 +332,7 @@ int sf_tm_destroy(sf_tm_t h) {
                   h->d_rewards, h->d_gids, h->d_cu,    h->d_adv,  h->d_total,   h->d_metrics};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  free_stages(h);
   for (int q = 0; q < h->xp_P; ++q)
     if (q != h->xp_rank && h->xp_mail[q]) cudaIpcCloseMemHandle(h->xp_mail[q]);
   if (h->xp_local) cudaFree(h->xp_local);
@@ -414,65 +495,72 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
   }
   if (tsum != T) return fail(h, SF_TM_CONFIG_ERROR, "sum(seq_lens) != T");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // grow-once scratch
-  if (int rc = ensure_tscratch(h, T)) return rc;
-  if (int rc = ensure_bscratch(h, B)) return rc;
-  if (int rc = ensure_cnt(h, B)) return rc;
+  // Pipelined prologue: the H2D of this micro-batch's bus fields and its
+  // varlen / GRPO / token-weight kernels run on the side stream, into the stage
+  // the loss two calls back has released, so they overlap the fused loss of
+  // the previous call on `s`; `s` then waits only for this stage to be ready.
+  sf_tm_handle::HostStage& g = h->st[h->st_next];
+  if (int rc = ensure_stage(h, g, T, B)) return rc;
+  cudaStream_t q = h->side;
+  cudaError_t e = cudaStreamWaitEvent(q, g.free_ev, 0);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sf_tm_pg_step_host");
   auto h2d = [&](void* d, const void* src, size_t bytes) {
-    return cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s);
+    return cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, q);
   };
-  cudaError_t e = cudaSuccess;
-  if ((e = h2d(h->d_targets, h_targets, sizeof(int32_t) * T)) ||
-      (e = h2d(h->d_old, h_old_logp, sizeof(float) * T)) ||
-      (e = h2d(h->d_ref, h_ref_logp, sizeof(float) * T)) ||
-      (e = h2d(h->d_lens, h_seq_lens, sizeof(int32_t) * B)) ||
-      (e = h2d(h->d_rewards, h_rewards, sizeof(float) * B)))
+  if ((e = h2d(g.targets, h_targets, sizeof(int32_t) * T)) ||
+      (e = h2d(g.old, h_old_logp, sizeof(float) * T)) ||
+      (e = h2d(g.ref, h_ref_logp, sizeof(float) * T)) ||
+      (e = h2d(g.lens, h_seq_lens, sizeof(int32_t) * B)) ||
+      (e = h2d(g.rewards, h_rewards, sizeof(float) * B)))
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
-  if (h_group_ids && (e = h2d(h->d_gids, h_group_ids, sizeof(int32_t) * B)))
+  if (h_group_ids && (e = h2d(g.gids, h_group_ids, sizeof(int32_t) * B)))
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
-  if (h_prompt_lens && (e = h2d(h->d_plens, h_prompt_lens, sizeof(int32_t) * B)))
+  if (h_prompt_lens && (e = h2d(g.plens, h_prompt_lens, sizeof(int32_t) * B)))
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
-  if (h_mask && (e = h2d(h->d_mask, h_mask, sizeof(uint8_t) * T)))
+  if (h_mask && (e = h2d(g.mask, h_mask, sizeof(uint8_t) * T)))
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
 
   int n = 0;
-  int rc = sftm::launch_varlen_meta(h->d_lens, h_prompt_lens ? h->d_plens : nullptr, nullptr, B, T,
-                                    h->d_cu, nullptr,
-                                    (!h_mask && h_prompt_lens) ? h->d_mask : nullptr, nullptr,
-                                    h->d_total, s, &n);
+  int rc = sftm::launch_varlen_meta(g.lens, h_prompt_lens ? g.plens : nullptr, nullptr, B, T, g.cu,
+                                    nullptr, (!h_mask && h_prompt_lens) ? g.mask : nullptr, nullptr,
+                                    g.total, q, &n);
   h->launches += n;
   if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host varlen");
-  const uint8_t* mask = (h_mask || h_prompt_lens) ? h->d_mask : nullptr;
-  const float* adv = h->d_rewards;
+  const uint8_t* mask = (h_mask || h_prompt_lens) ? g.mask : nullptr;
+  const float* adv = g.rewards;
   if (adv_eps >= 0.f) {
     n = 0;
-    rc = sftm::launch_grpo_advantage(h->d_rewards, h->d_gids, B, adv_eps, std_mode, h->d_adv,
-                                     nullptr, s, &n);
+    rc = sftm::launch_grpo_advantage(g.rewards, g.gids, B, adv_eps, std_mode, g.adv, nullptr, q, &n);
     h->launches += n;
     if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host advantage");
-    adv = h->d_adv;
+    adv = g.adv;
   }
   n = 0;
-  rc = sftm::launch_token_weights(h->d_cu, B, adv, mask, T, params->norm_mode, params->inv_norm,
-                                  h->d_advtok, h->d_wtok, h->cnt, h->ticket2, h->tot, s, &n);
+  rc = sftm::launch_token_weights(g.cu, B, adv, mask, T, params->norm_mode, params->inv_norm, g.advtok,
+                                  g.wtok, g.cnt, g.ticket, g.tot, q, &n);
   h->launches += n;
   if (rc) return cuda_fail(h, rc, "sf_tm_pg_step_host token weights");
+  if ((e = cudaEventRecord(g.ready_ev, q)) || (e = cudaStreamWaitEvent(s, g.ready_ev, 0)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host");
   sftm::RowArgs a;
   a.logits = logits;
   a.dtype = dtype;
   a.T = T;
   a.V = V;
   a.ld = ld;
-  a.targets = h->d_targets;
-  a.old_logp = h->d_old;
-  a.ref_logp = h->d_ref;
-  a.adv_tok = h->d_advtok;
-  a.w_tok = h->d_wtok;
+  a.targets = g.targets;
+  a.old_logp = g.old;
+  a.ref_logp = g.ref;
+  a.adv_tok = g.advtok;
+  a.w_tok = g.wtok;
   fill_loss(a, params);
   a.dlogits = dlogits;
   a.ld_d = ld_d;
   a.out_metrics = h->d_metrics;
   if (int r2 = run_rows(h, a, sftm::kModeFwdBwd, s, "sf_tm_pg_step_host loss")) return r2;
+  if ((e = cudaEventRecord(g.free_ev, s)))
+    return cuda_fail(h, e, "sf_tm_pg_step_host");
+  h->st_next ^= 1;
   e = cudaMemcpyAsync(h_metrics, h->d_metrics, sizeof(float) * SF_TM_NUM_METRICS,
                       cudaMemcpyDeviceToHost, s);
   return check_cuda(h, e, "sf_tm_pg_step_host D2H");

@@ -440,6 +440,37 @@ def test_pg_step_host_matches_oracle_pipeline(tm, orc):
         assert_close(gm[:6], om[:6], atol=2e-5, rtol=1e-4, what="metrics")
 
 
+def test_pg_step_host_pipelined_calls_match_synced(tm, orc):
+    """Back-to-back seam calls (no sync between them) overlap each call's H2D and
+    prologue with the previous call's loss in two alternating stages; results
+    must equal the same calls made one at a time (stage reuse, stage growth,
+    masks on/off, precomputed advantages)."""
+    pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()
+    probs = [orc.synth_problem(40 + i, lens, 32000, "bf16", prompt_max=20, G=2)
+             for i, lens in enumerate([[30, 22], [64, 40, 9, 17], [300, 210, 5, 90, 77, 64], [12, 12],
+                                       [500, 400], [33, 1, 70, 2]])]
+
+    def call(i, p, x):
+        args = [pin(p["targets"], np.int32), pin(p["old"], np.float32), pin(p["ref"], np.float32),
+                pin(p["lens"], np.int32), pin(p["rewards"], np.float32), pin(p["gids"], np.int32)]
+        kw = dict(h_prompt_lens=pin(p["plens"], np.int32)) if i % 3 != 2 else {}
+        eps = -1.0 if i == 3 else 1e-6  # call 3: rewards taken as precomputed advantages
+        return tm.pg_step_host(x, *args, adv_eps=eps, **kw)
+
+    xs = [to_dev_logits(p) for p in probs]
+    ref = []
+    for i, (p, x) in enumerate(zip(probs, xs)):
+        hm, dl = call(i, p, x)
+        torch.cuda.synchronize()
+        ref.append((hm.clone(), dl.clone()))
+    for rep in range(2):
+        outs = [call(i, p, x) for i, (p, x) in enumerate(zip(probs, xs))]
+        torch.cuda.synchronize()
+        for i, ((hm, dl), (rm, rd)) in enumerate(zip(outs, ref)):
+            assert torch.equal(hm, rm), (rep, i)
+            assert torch.equal(dl, rd), (rep, i)
+
+
 # ---------------------------------------------------------------------------- a7 vocab parallel (1-GPU emulation)
 @pytest.mark.parametrize("P", [2, 4])
 def test_vocab_parallel_matches_fused(tm, orc, P):
