@@ -215,7 +215,13 @@ int sf_tm_pg_loss_fwd_bwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t 
  *   h_targets[T], h_old_logp[T], h_ref_logp[T]: packed per-token fields;
  *   h_seq_lens[B], h_prompt_lens[B] (optional), h_rewards[B], h_group_ids[B];
  *   h_mask[T] (optional; overrides prompt_lens-derived mask).
- * If adv_eps < 0 the rewards are taken as precomputed advantages. */
+ * If adv_eps < 0 the rewards are taken as precomputed advantages.
+ * Pipelined: the H2D copies and the varlen / GRPO / token-weight kernels run on
+ * a handle-owned side stream (two alternating scratch stages), overlapping the
+ * previous call's fused loss on `stream`; `stream` waits for them before the
+ * loss. Back-to-back calls need no synchronisation between them, but the host
+ * input buffers stay in use until sf_tm_wait_host_inputs returns (or `stream`
+ * is synchronised). */
 int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
                        int64_t ld, const int32_t* h_targets, const float* h_old_logp,
                        const float* h_ref_logp, const uint8_t* h_mask, const int32_t* h_seq_lens,
@@ -223,6 +229,11 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
                        const int32_t* h_group_ids, int64_t B, float adv_eps, int32_t std_mode,
                        const sf_tm_loss_params* params, void* dlogits, int64_t ld_d,
                        float* h_metrics, void* stream);
+
+/* Blocks until the host input buffers of every sf_tm_pg_step_host call made
+ * on this handle so far have been read (their H2D copies are complete), so the
+ * caller may refill them. Does not wait for the loss itself. */
+int sf_tm_wait_host_inputs(sf_tm_t h);
 
 /* ---- a5: R3 rollout routing replay gate ---------------------------------
  * router_logits[L*T, E] (dtype), rec_idx[L*T, k] (SF_TM_IDX_I32 / _U8).

@@ -207,7 +207,8 @@ class ActorLossSeam {
 
   // Decode `batch`, copy its bus fields through pinned staging, and run the
   // fused DAPO/GRPO loss fwd+bwd on `d_logits` [T, V] (row stride V). Writes
-  // dlogits and the metrics (valid once `stream` is synchronised). When the
+  // dlogits and the metrics (valid once `stream` is synchronised; steps may be
+  // issued back to back, the next one overlapping this one's loss). When the
   // batch carries rewards (GRPO computed here), every group must be complete
   // in the micro-batch unless allow_partial_groups.
   template <class MicroBatchT>
@@ -224,6 +225,9 @@ class ActorLossSeam {
       return rc;
     }
     const PackedBatch& p = packed_;
+    // the previous step's H2D may still be reading the pinned staging (calls
+    // are pipelined; no stream sync is required between steps)
+    if ((rc = sf_tm_wait_host_inputs(h_))) return rc;
     if ((rc = stage(0, p.targets.data(), p.targets.size() * 4)) || (rc = stage(1, p.logp.data(), p.T * 4)) ||
         (rc = stage(2, p.ref_logp.data(), p.T * 4)) || (rc = stage(3, p.seq_lens.data(), p.B * 4)) ||
         (rc = stage(4, p.per_sample.data(), p.B * 4)) || (rc = stage(5, p.group_ids.data(), p.B * 4)))

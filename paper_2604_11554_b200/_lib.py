@@ -95,6 +95,7 @@ _SIGS = {
          ctypes.POINTER(LossParams), _vp, _i64, _vp, _vp, _vp, _vp],
     ),
     "sf_tm_sync": (ctypes.c_int, [_H, _vp]),
+    "sf_tm_wait_host_inputs": (ctypes.c_int, [_H]),
     "sf_tm_logprob_fwd_host": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp]),
     "sf_tm_grpo_advantage_host": (ctypes.c_int, [_H, _vp, _vp, _i64, _f32, _i32, _vp, _vp]),
     "sf_tm_vp_mailbox_create": (ctypes.c_int, [_H, _i32, _i32, _vp]),

@@ -81,6 +81,7 @@ struct sf_tm_handle {
   } st[2];
   int st_next = 0;
   cudaStream_t side = nullptr;
+  cudaEvent_t h2d_ev = nullptr;  // after the latest call's host-input copies (side stream)
 };
 
 namespace {
@@ -221,6 +222,7 @@ int ensure_bscratch(sf_tm_t h, int64_t B) {
 int ensure_stage(sf_tm_t h, sf_tm_handle::HostStage& g, int64_t T, int64_t B) {
   if (!h->side) {
     cudaError_t e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->h2d_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(h, e, "pg_step_host side stream");
   }
   if (!g.ready_ev) {
@@ -266,6 +268,7 @@ void free_stages(sf_tm_t h) {
     if (g.ready_ev) cudaEventDestroy(g.ready_ev);
     if (g.free_ev) cudaEventDestroy(g.free_ev);
   }
+  if (h->h2d_ev) cudaEventDestroy(h->h2d_ev);
   if (h->side) cudaStreamDestroy(h->side);
 }
 
@@ -519,6 +522,7 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
   if (h_mask && (e = h2d(g.mask, h_mask, sizeof(uint8_t) * T)))
     return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
+  if ((e = cudaEventRecord(h->h2d_ev, q))) return cuda_fail(h, e, "sf_tm_pg_step_host H2D");
 
   int n = 0;
   int rc = sftm::launch_varlen_meta(g.lens, h_prompt_lens ? g.plens : nullptr, nullptr, B, T, g.cu,
@@ -564,6 +568,13 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
   e = cudaMemcpyAsync(h_metrics, h->d_metrics, sizeof(float) * SF_TM_NUM_METRICS,
                       cudaMemcpyDeviceToHost, s);
   return check_cuda(h, e, "sf_tm_pg_step_host D2H");
+}
+
+int sf_tm_wait_host_inputs(sf_tm_t h) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (!h->h2d_ev) return SF_TM_OK;  // no pg_step_host call yet
+  if (int rc = use_device(h)) return rc;
+  return check_cuda(h, cudaEventSynchronize(h->h2d_ev), "sf_tm_wait_host_inputs");
 }
 
 int sf_tm_sync(sf_tm_t h, void* stream) {

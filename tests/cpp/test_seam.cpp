@@ -191,6 +191,44 @@ void test_gpu() {
   cudaFree(logits);
   cudaFree(dl1);
   cudaFree(dl2);
+  // back-to-back steps (no sync between them: the seam refills its pinned
+  // staging only after the previous step's H2D has read it) == synced steps
+  {
+    const int nb = 4;
+    std::vector<MicroBatch> bs;
+    std::vector<int64_t> Ts;
+    std::vector<void*> lg(nb), da(nb), db(nb);
+    std::vector<std::vector<float>> ma(nb, std::vector<float>(SF_TM_NUM_METRICS)),
+        mb(nb, std::vector<float>(SF_TM_NUM_METRICS));
+    for (int i = 0; i < nb; ++i) {
+      bs.push_back(make_batch(V, 8 + 4 * i, 120 + 60 * i, 21 + i, false));
+      staleflow::train_math::PackedBatch q;
+      staleflow::train_math::pack_trainer_batch(bs[i], 4, q, &err);
+      Ts.push_back(q.T);
+      cudaMalloc(&lg[i], q.T * V * 2);
+      cudaMalloc(&da[i], q.T * V * 2);
+      cudaMalloc(&db[i], q.T * V * 2);
+      CHECK(sf_tm_synth_logits(seam.handle(), lg[i], SF_TM_BF16, q.T, V, V, 30 + i, 2.f, nullptr, 0.f, 0.f, 1e-3f,
+                               nullptr) == SF_TM_OK);
+    }
+    for (int i = 0; i < nb; ++i) {
+      CHECK(seam.step(bs[i], lg[i], SF_TM_BF16, V, da[i], prm, ma[i].data(), nullptr, 4) == SF_TM_OK);
+      cudaDeviceSynchronize();
+    }
+    for (int i = 0; i < nb; ++i)
+      CHECK(seam.step(bs[i], lg[i], SF_TM_BF16, V, db[i], prm, mb[i].data(), nullptr, 4) == SF_TM_OK);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < nb; ++i) {
+      CHECK(ma[i] == mb[i]);
+      std::vector<unsigned char> ha(Ts[i] * V * 2), hb(Ts[i] * V * 2);
+      cudaMemcpy(ha.data(), da[i], ha.size(), cudaMemcpyDeviceToHost);
+      cudaMemcpy(hb.data(), db[i], hb.size(), cudaMemcpyDeviceToHost);
+      CHECK(ha == hb);
+      cudaFree(lg[i]);
+      cudaFree(da[i]);
+      cudaFree(db[i]);
+    }
+  }
   // routed_experts codec -> R3 gate: the replayed indices are the decoded record, bit for bit
   {
     const int layers = 4, k = 8, E = 128;
