@@ -985,8 +985,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int p = 0; p < NE / 2; ++p) {
             if ((2 * p < EV) ? vok0 : vok1) {
               const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
-              gr[2 * p] = ex2(av.x);
-              gr[2 * p + 1] = ex2(av.y);
+#ifdef SFTM_POLY_EXP
+              if (p < SFTM_POLY_EXP) {  // A/B: this pair's exponentials on the FMA pipe
+                const float2 e2 = ex2_poly2(av);
+                gr[2 * p] = e2.x;
+                gr[2 * p + 1] = e2.y;
+              } else
+#endif
+              {
+                gr[2 * p] = ex2(av.x);
+                gr[2 * p + 1] = ex2(av.y);
+              }
             } else {
               gr[2 * p] = gr[2 * p + 1] = 0.f;
             }
