@@ -381,7 +381,21 @@ __global__ void __launch_bounds__(256, (E / G <= 16) ? 4 : 2)
       n_ge = gsumi_g<G>(n_ge);
       bool mm = grp_bad;
       const bool slow = !grp_bad && n_ge > k;
+      // At most k - 1 recorded experts lie strictly above in_min (one of them is
+      // the minimum), so k experts strictly above it prove a mismatch: no
+      // membership needed. Only exact ties at in_min take the per-expert path.
+      bool tie = false;
       if (__any_sync(0xffffffffu, slow)) {
+        int n_gt = 0;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) n_gt += z[i][c] > in_min ? 1 : 0;
+        n_gt = gsumi_g<G>(n_gt);
+        if (slow && n_gt >= k) mm = true;
+        tie = slow && n_gt < k;
+      }
+      if (__any_sync(0xffffffffu, tie)) {
         // membership of my experts in the recorded set (k <= G, unrolled)
         uint32_t mine = 0;
 #pragma unroll
@@ -414,7 +428,7 @@ __global__ void __launch_bounds__(256, (E / G <= 16) ? 4 : 2)
           in_hi = max(in_hi, __shfl_xor_sync(0xffffffffu, in_hi, o, G));
           out_lo = min(out_lo, __shfl_xor_sync(0xffffffffu, out_lo, o, G));
         }
-        if (slow && (out_max > in_min || (out_max == in_min && out_lo < in_hi))) mm = true;
+        if (tie && (out_max > in_min || (out_max == in_min && out_lo < in_hi))) mm = true;
       }
       // per-layer counts; the layer boundary advances incrementally (no 64-bit division per row)
       const unsigned bal = __ballot_sync(0xffffffffu, valid && mm && gl == 0);

@@ -526,11 +526,15 @@ def test_r3_gate(tm, orc, dtype, idx_dtype, renorm, E, k):
     else:
         zin, zt = z, torch.from_numpy(z).cuda()
     z[1, :3] = 0.0  # fully tied rows (P9)
+    z[3, 100:200] = np.round(z[3, 100:200] / 2)  # coarse logits: many exact ties at the k-th value
     if dtype == "bf16":
         zin[1, :3] = 0
         zt[1, :3] = 0
+        zin[3, 100:200] = orc.f32_to_bf16_bits(z[3, 100:200]).reshape(100, E)
+        zt[3, 100:200] = torch.from_numpy(z[3, 100:200]).to(torch.bfloat16).cuda()
     else:
         zt[1, :3] = 0
+        zt[3, 100:200] = torch.from_numpy(z[3, 100:200]).cuda()
     order = np.lexsort((np.broadcast_to(np.arange(E), z.shape), -z), axis=-1)
     rec = order[..., :k].copy()
     flip = rng.random((L, T)) < 0.05
@@ -539,6 +543,8 @@ def test_r3_gate(tm, orc, dtype, idx_dtype, renorm, E, k):
         rec[l, t, rng.integers(0, k)] = rng.choice(others)
     rec[2, :4, 1] = rec[2, :4, 0]  # duplicated recorded expert: not a top-k set (mismatch)
     rec[1, 3:6] = order[1, 3:6, 1:k + 1]  # shifted by one: a boundary swap
+    rec[3, 100:200:3, k - 1] = order[3, 100:200:3, k]  # tied rows: swap in the next expert in
+    # (logit desc, index asc) order -- an equal logit at a higher index is still a mismatch (P9)
     rec = rec.astype(np.uint8 if idx_dtype == "u8" else np.int32)
     rt = torch.from_numpy(rec).cuda()
     w, idx, mm = tm.r3_gate_fwd(zt, rt, renorm=renorm)
