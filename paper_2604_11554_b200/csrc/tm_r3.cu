@@ -16,6 +16,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+#include <cstdlib>
+
 #include "tm_device.cuh"
 #include "tm_internal.h"
 
@@ -514,6 +517,103 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// k = 8 backward: the loop body has no global loads. A warp takes chunks of 16
+// rows; their (index, w, dw) are one 16-B load each per lane (lane l holds
+// row l/2, entries 4(l&1)..+3), prefetched a whole chunk (8 two-row
+// iterations) ahead, so the metadata latency is hidden behind the dense store
+// stream. Each iteration: zero two row buffers, the four lanes holding the two
+// rows scatter w_j (dw_j - S) into them, then every lane stores 16-B vectors.
+template <typename T, int NB, int VAR>
+__global__ void __launch_bounds__(256)
+    r3_bwd_k8(int64_t rows, const void* __restrict__ rec, int idx_dtype, const float* __restrict__ w,
+              const float* __restrict__ dw, T* __restrict__ dz) {
+  constexpr int E = NB * 64;
+  __shared__ __align__(16) float buf[8][2][E];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gl = lane & 15, half = lane >> 4;
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nchunk = (rows + 15) / 16;
+  auto load = [&](int64_t c, float4& wv, float4& dv, int4& ev) {
+    const int64_t r = c * 16 + (lane >> 1);
+    if (c < nchunk && r < rows) {
+      const int64_t o = r * 8 + 4 * (lane & 1);
+      wv = __ldg(reinterpret_cast<const float4*>(w + o));
+      dv = __ldg(reinterpret_cast<const float4*>(dw + o));
+      if (idx_dtype == 1) {
+        const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(rec) + o));
+        ev = make_int4(u & 255u, (u >> 8) & 255u, (u >> 16) & 255u, u >> 24);
+      } else {
+        ev = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(rec) + o));
+      }
+    } else {
+      wv = dv = make_float4(0.f, 0.f, 0.f, 0.f);
+      ev = make_int4(-1, -1, -1, -1);
+    }
+  };
+  float4 wv, dv;
+  int4 ev;
+  load(gw, wv, dv, ev);
+  if (VAR >= 1) {  // buffers zeroed once; each iteration resets only the entries it set
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      *reinterpret_cast<float4*>(buf[wid][half] + i * 64 + 4 * gl) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+  }
+  for (int64_t c = gw; c < nchunk; c += nw) {
+    float4 wn, dn;
+    int4 en;
+    load(c + nw, wn, dn, en);
+    float S = wv.x * dv.x + wv.y * dv.y + wv.z * dv.z + wv.w * dv.w;
+    S += __shfl_xor_sync(0xffffffffu, S, 1);
+    const float v0 = wv.x * (dv.x - S), v1 = wv.y * (dv.y - S), v2 = wv.z * (dv.z - S), v3 = wv.w * (dv.w - S);
+    float* rb = buf[wid][half];
+    float* tb = buf[wid][(lane >> 1) & 1];  // the buffer of the row this lane's entries belong to
+#pragma unroll 1
+    for (int it = 0; it < 8; ++it) {
+      const int64_t row = c * 16 + 2 * it + half;
+      if (VAR == 0) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) *reinterpret_cast<float4*>(rb + i * 64 + 4 * gl) = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+      }
+      if ((lane >> 2) == it) {  // duplicates of a recorded expert accumulate
+        if (ev.x >= 0 && ev.x < E) atomicAdd(tb + ev.x, v0);
+        if (ev.y >= 0 && ev.y < E) atomicAdd(tb + ev.y, v1);
+        if (ev.z >= 0 && ev.z < E) atomicAdd(tb + ev.z, v2);
+        if (ev.w >= 0 && ev.w < E) atomicAdd(tb + ev.w, v3);
+      }
+      __syncwarp();
+      if (row < rows) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const float4 o = *reinterpret_cast<const float4*>(rb + i * 64 + 4 * gl);
+          T* d = dz + row * E + i * 64 + 4 * gl;
+          if constexpr (sizeof(T) == 4) {
+            if (VAR == 2) __stcs(reinterpret_cast<float4*>(d), o);
+            else *reinterpret_cast<float4*>(d) = o;
+          } else {
+            const uint2 pk = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+            if (VAR == 2) __stcs(reinterpret_cast<uint2*>(d), pk);
+            else *reinterpret_cast<uint2*>(d) = pk;
+          }
+        }
+      }
+      __syncwarp();
+      if (VAR >= 1 && (lane >> 2) == it) {
+        if (ev.x >= 0 && ev.x < E) tb[ev.x] = 0.f;
+        if (ev.y >= 0 && ev.y < E) tb[ev.y] = 0.f;
+        if (ev.z >= 0 && ev.z < E) tb[ev.z] = 0.f;
+        if (ev.w >= 0 && ev.w < E) tb[ev.w] = 0.f;
+      }
+      if (VAR >= 1) __syncwarp();
+    }
+    wv = wn;
+    dv = dn;
+    ev = en;
+  }
+}
+
 namespace {
 int r3_grid(int64_t rows) {
   int dev = 0, sms = 148;
@@ -577,6 +677,50 @@ int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E
                   const void* rec_idx, int idx_dtype, int renorm, const float* w, const float* dw,
                   void* dlogits, cudaStream_t s, int* launches) {
   const int64_t rows = L * T;
+  const bool al = (reinterpret_cast<uintptr_t>(w) % 16 == 0) && (reinterpret_cast<uintptr_t>(dw) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(rec_idx) % (idx_dtype == 1 ? 4 : 16) == 0);
+  if (renorm && k == 8 && E % 64 == 0 && E <= 256 && al && !getenv("SFTM_R3_BWD_OLD")) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // one resident wave (grid-stride over 16-row chunks): no tail wave
+    auto grid_for = [&](const void* fn) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      int64_t g = ((rows + 15) / 16 + 7) / 8;
+      if (g > static_cast<int64_t>(sms) * per_sm) g = static_cast<int64_t>(sms) * per_sm;
+      return static_cast<int>(g < 1 ? 1 : g);
+    };
+    const char* vs = getenv("SFTM_R3_BWD_VAR");  // A/B only
+    const int var = vs ? atoi(vs) : 1;  // 1: reset the touched entries (0: zero-fill, 0.667 -> 0.625 ms)
+#define LAUNCH_B8V(NB, V)                                                                             \
+  if (dtype == 1)                                                                                     \
+    r3_bwd_k8<uint16_t, NB, V><<<grid_for(reinterpret_cast<const void*>(&r3_bwd_k8<uint16_t, NB, V>)), \
+                                 256, 0, s>>>(rows, rec_idx, idx_dtype, w, dw,                        \
+                                              static_cast<uint16_t*>(dlogits));                       \
+  else                                                                                                \
+    r3_bwd_k8<float, NB, V><<<grid_for(reinterpret_cast<const void*>(&r3_bwd_k8<float, NB, V>)), 256, \
+                              0, s>>>(rows, rec_idx, idx_dtype, w, dw, static_cast<float*>(dlogits));
+#define LAUNCH_B8(NB)          \
+  if (var == 1) {              \
+    LAUNCH_B8V(NB, 1)          \
+  } else if (var == 2) {       \
+    LAUNCH_B8V(NB, 2)          \
+  } else {                     \
+    LAUNCH_B8V(NB, 0)          \
+  }
+    switch (E / 64) {
+      case 1: LAUNCH_B8(1) break;
+      case 2: LAUNCH_B8(2) break;
+      case 3: LAUNCH_B8(3) break;
+      default: LAUNCH_B8(4) break;
+    }
+#undef LAUNCH_B8
+#undef LAUNCH_B8V
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   if (renorm && E % 64 == 0 && E <= 256 && k <= 16) {
     const int g2 = r3_grid((rows + 1) / 2);
 #define LAUNCH_BF(NB)                                                                                  \
