@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(256)
 // k = 8 backward: the loop body has no global loads. A warp takes chunks of 16
 // rows; their (index, w, dw) are one 16-B load each per lane (lane l holds
 // row l/2, entries 4(l&1)..+3), prefetched a whole chunk (8 two-row
-// iterations) ahead. Each iteration the four lanes holding the two rows scatter
+// iterations) ahead. Each iteration the four lanes holding the two rows add
 // w_j (dw_j - S) into two zeroed smem row buffers, every lane stores its 16-B
 // vectors, and the scattering lanes reset only the entries they set (measured:
 // 0.625 ms vs 0.667 ms re-zeroing the whole rows; also tried and slower: an
@@ -574,13 +574,19 @@ __global__ void __launch_bounds__(256)
     for (int it = 0; it < 8; ++it) {
       const int64_t row = c * 16 + 2 * it + half;
       const bool mine = (lane >> 2) == it;
-      if (mine) {  // duplicates of a recorded expert accumulate
-        if (ok0) atomicAdd(tb + ev.x, v0);
-        if (ok1) atomicAdd(tb + ev.y, v1);
-        if (ok2) atomicAdd(tb + ev.z, v2);
-        if (ok3) atomicAdd(tb + ev.w, v3);
+      // plain read-add-write, the row's two lanes one after the other: duplicates of
+      // a recorded expert accumulate without shared-memory float atomics (a CAS loop
+      // on sm_100a)
+#pragma unroll
+      for (int ph = 0; ph < 2; ++ph) {
+        if (mine && (lane & 1) == ph) {
+          if (ok0) tb[ev.x] += v0;
+          if (ok1) tb[ev.y] += v1;
+          if (ok2) tb[ev.z] += v2;
+          if (ok3) tb[ev.w] += v3;
+        }
+        __syncwarp();
       }
-      __syncwarp();
       if (row < rows) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
