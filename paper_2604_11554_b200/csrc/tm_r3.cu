@@ -321,16 +321,24 @@ __global__ void __launch_bounds__(256, (E / G <= 16) ? 4 : 2)
   if (p1 > steps) p1 = steps;
   int64_t cur_layer = 0, layer_end = -1;  // forces a (single) division on the first row
   uint32_t cur_cnt = 0;
+  // the recorded index is prefetched one step ahead: the recorded logit's load
+  // depends on it, and waiting for it was the kernel's main stall (ncu source page)
+  auto idx_of = [&](int64_t q) {
+    const int64_t r = R * q + gi;
+    return gl < k ? r3_idx(rec, idx_dtype, (r < rows ? r : rows - 1) * k + gl) : -1;
+  };
+  int e_next = p0 < p1 ? idx_of(p0) : -1;
   for (int64_t pr = p0; pr < p1; ++pr) {
     const int64_t row = R * pr + gi;
     const bool valid = row < rows;
     const int64_t rowc = valid ? row : rows - 1;
     float z[NV][4];
-    // no software prefetch: a lean register budget keeps 4 CTAs (32 warps) per
-    // SM resident, which hides the load latency better (measured: 0.62 vs 0.76 ms)
+    // no software prefetch of the logits: a lean register budget keeps 4 CTAs
+    // (32 warps) per SM resident, which hides their latency better (0.62 vs 0.76 ms)
 #pragma unroll
     for (int i = 0; i < NV; ++i) r3_load4(logits + rowc * E + i * W + 4 * gl, z[i]);
-    const int my_e = gl < k ? r3_idx(rec, idx_dtype, rowc * k + gl) : -1;
+    const int my_e = e_next;
+    if (pr + 1 < p1) e_next = idx_of(pr + 1);
     float zr = -INFINITY;
     if (gl < k) {
       // the recorded logit: an L1 hit (the row's lines were just loaded)
