@@ -126,8 +126,8 @@ int sf_tm_abi_version(void);
 uint64_t sf_tm_launch_count(sf_tm_t h);
 /* Which row kernel the last row-kernel call on this handle launched:
  * *kernel 0 = streaming TMA ring, 1 = generic two-pass, 2 = fused TMEM/smem
- * row-store loss kernel, 3 = its per-warp pipelined variant, 4 = the fused
- * vocab-parallel (peer-mailbox) kernel, 5 = the forward-only streaming kernel; *cluster = CTAs
+ * row-store loss kernel, 4 = the fused vocab-parallel (peer-mailbox) kernel,
+ * 5 = the forward-only streaming kernel; *cluster = CTAs
  * per row; *grid = CTAs launched. Any pointer may be NULL. */
 int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* grid);
 
@@ -289,8 +289,14 @@ int sf_tm_vp_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dtype, in
  * Then every rank calls sf_tm_vp_fused_loss_fwd_bwd with the same T, w_tok and
  * call sequence (calls are matched by order). Outputs are as
  * sf_tm_vp_loss_fwd_bwd; metrics, logp and entropy are identical on all ranks.
- * A rank whose peers never launch traps after SF_TM_XP_TIMEOUT_S seconds
- * (environment, default 300) instead of hanging silently. */
+ * A call that returns an error before launching does not advance the call
+ * sequence; since shapes and pointers may differ per rank, a caller should
+ * first agree on sf_tm_vp_fused_check across the group (e.g. an all-reduce
+ * of the result) and use the two-pass form on every rank if any rank fails.
+ * A launch whose peers never launch stops waiting after SF_TM_XP_TIMEOUT_S
+ * seconds (environment, default 300), finishes with invalid outputs and
+ * flags the handle: every later fused call on it returns SF_TM_INTERNAL. The
+ * CUDA context stays usable (no trap). */
 #define SF_TM_IPC_HANDLE_BYTES 64
 int sf_tm_vp_mailbox_create(sf_tm_t h, int32_t P, int32_t rank, void* ipc_handle_out);
 int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles);
@@ -299,6 +305,12 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
                                 const float* ref_logp, const float* adv_tok, const float* w_tok,
                                 const sf_tm_loss_params* params, void* dlogits, int64_t ld_d, float* out_metrics,
                                 float* out_logp, float* out_entropy, void* stream);
+
+/* The checks sf_tm_vp_fused_loss_fwd_bwd makes on its shard (mailboxes open
+ * and healthy, dtype, 16-B aligned rows/widths/strides, shard row fits one
+ * CTA's row store), with no side effect. Ok or ConfigError / Internal. */
+int sf_tm_vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp, int64_t ld,
+                         const void* dlogits, int64_t ld_d);
 
 /* ---- pinned host staging (for the C++ seam adapter) ----------------------
  * Page-locked host memory so the seam's H2D copies are asynchronous DMA.
@@ -321,6 +333,13 @@ int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_
  * on != 0 routes all row kernels to the generic two-pass (non-TMA) kernel so
  * tests can cover both code paths; process-wide. Not for production use. */
 int sf_tm_debug_force_generic(int on);
+
+/* Wires P handles on ONE device into an in-process vocab-parallel group
+ * (rank r = handles[r]) without CUDA IPC, and caps each rank's exchange grid
+ * at grid_per_rank CTAs (0 = no cap) so the P ranks' kernels, launched on P
+ * streams, are co-resident on the GPU. Emulates P GPUs on one for tests and
+ * the narrow-shard measurement; not for production use. */
+int sf_tm_debug_vp_local_group(sf_tm_t* handles, int32_t P, int32_t grid_per_rank);
 
 /* on a non-NULL device buffer of 16 uint64 (zeroed by the caller), the fused
  * loss kernel accumulates per-role clock64 cycle sums: for role r in

@@ -105,6 +105,8 @@ _SIGS = {
         [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
          ctypes.POINTER(LossParams), _vp, _i64, _vp, _vp, _vp, _vp],
     ),
+    "sf_tm_vp_fused_check": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _vp, _i64]),
+    "sf_tm_debug_vp_local_group": (ctypes.c_int, [ctypes.POINTER(_H), _i32, _i32]),
     "sf_tm_synth_logits": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _u64, _f32, _vp, _f32, _f32, _f32, _vp]),
     "sf_tm_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "sf_tm_host_free": (ctypes.c_int, [_vp]),

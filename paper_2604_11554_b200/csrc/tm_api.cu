@@ -27,8 +27,12 @@ struct sf_tm_handle {
   void* xp_mail[sftm::kXpMaxP] = {};
   int xp_P = 0, xp_rank = -1;
   bool xp_ready = false;
+  bool xp_local_group = false;  // peers wired in-process (sf_tm_debug_vp_local_group)
   unsigned long long xp_epoch = 0;
-  int* xp_err = nullptr;
+  int* xp_err_h = nullptr;  // host-mapped launch-failure word (peer timeout)
+  int* xp_err_d = nullptr;  // its device alias
+  int* xp_abort = nullptr;  // device: stop-waiting flag shared by a launch's CTAs
+  int xp_grid = 0;
   // metric partials for the deterministic row-kernel reduction
   double* partials = nullptr;
   unsigned* ticket = nullptr;
@@ -272,6 +276,45 @@ void free_stages(sf_tm_t h) {
   if (h->side) cudaStreamDestroy(h->side);
 }
 
+// This rank's mailbox, the host-mapped failure word and the abort flag.
+int alloc_mailbox(sf_tm_t h, int32_t P, int32_t rank) {
+  cudaError_t e = cudaMalloc(&h->xp_local, sftm::kXpMailboxBytes);
+  if (e == cudaSuccess) e = cudaMemset(h->xp_local, 0, sftm::kXpMailboxBytes);
+  if (e == cudaSuccess) e = cudaMalloc(&h->xp_abort, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(h->xp_abort, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&h->xp_err_h), sizeof(int), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *h->xp_err_h = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->xp_err_d), h->xp_err_h, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return check_cuda(h, e, "peer mailbox");
+  h->xp_P = P;
+  h->xp_rank = rank;
+  h->xp_mail[rank] = h->xp_local;
+  return SF_TM_OK;
+}
+
+// Everything sf_tm_vp_fused_loss_fwd_bwd checks before it consumes a launch
+// epoch: a call that fails here has no effect on the peers' call sequence.
+int vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp, int64_t ld,
+                   const void* dlogits, int64_t ld_d) {
+  if (!h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "peer mailboxes not open (sf_tm_vp_mailbox_open)");
+  if (*h->xp_err_h)
+    return fail(h, SF_TM_INTERNAL,
+                "an earlier fused vocab-parallel launch timed out waiting for a peer (its outputs are invalid); "
+                "the peer exchange of this handle is disabled, use sf_tm_vp_loss_fwd_bwd");
+  if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
+  if (T < 0 || Vp <= 0 || ld < Vp || ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "bad shard shape or stride");
+  const int64_t es = dtype == SF_TM_BF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(logits_shard) | reinterpret_cast<uintptr_t>(dlogits)) % 16 ||
+      (ld * es) % 16 || (ld_d * es) % 16 || (Vp * es) % 16)
+    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows, widths and strides");
+  if (!sftm::loss_xp_eligible(dtype, Vp))
+    return fail(h, SF_TM_CONFIG_ERROR, "shard row too wide for the fused vocab-parallel kernel");
+  return SF_TM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -336,10 +379,12 @@ int sf_tm_destroy(sf_tm_t h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   free_stages(h);
-  for (int q = 0; q < h->xp_P; ++q)
-    if (q != h->xp_rank && h->xp_mail[q]) cudaIpcCloseMemHandle(h->xp_mail[q]);
+  if (!h->xp_local_group)
+    for (int q = 0; q < h->xp_P; ++q)
+      if (q != h->xp_rank && h->xp_mail[q]) cudaIpcCloseMemHandle(h->xp_mail[q]);
   if (h->xp_local) cudaFree(h->xp_local);
-  if (h->xp_err) cudaFree(h->xp_err);
+  if (h->xp_abort) cudaFree(h->xp_abort);
+  if (h->xp_err_h) cudaFreeHost(h->xp_err_h);
   delete h;
   return SF_TM_OK;
 }
@@ -488,6 +533,9 @@ int sf_tm_pg_step_host(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, 
   if (B <= 0) return fail(h, SF_TM_CONFIG_ERROR, "B must be > 0");
   if (!h_seq_lens || !h_rewards || !h_metrics || !h_old_logp || !h_ref_logp || !dlogits)
     return fail(h, SF_TM_CONFIG_ERROR, "missing required host buffer");
+  if (ld_d < V) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= V");
+  if (dlogits == logits && ld_d != ld)
+    return fail(h, SF_TM_CONFIG_ERROR, "in-place dlogits needs ld_d == ld");
   if (adv_eps >= 0.f && !h_group_ids)
     return fail(h, SF_TM_CONFIG_ERROR, "group ids are required to compute advantages");
   if (std_mode < 0 || std_mode > 2) return fail(h, SF_TM_CONFIG_ERROR, "std_mode must be SF_TM_STD_*");
@@ -762,18 +810,11 @@ int sf_tm_vp_mailbox_create(sf_tm_t h, int32_t P, int32_t rank, void* ipc_handle
   if (rank < 0 || rank >= P) return fail(h, SF_TM_CONFIG_ERROR, "rank must be in [0, P)");
   if (!ipc_handle_out) return fail(h, SF_TM_CONFIG_ERROR, "ipc_handle_out is required");
   if (h->xp_local) return fail(h, SF_TM_CONFIG_ERROR, "mailbox already created on this handle");
-  cudaError_t e = cudaMalloc(&h->xp_local, sftm::kXpMailboxBytes);
-  if (e == cudaSuccess) e = cudaMemset(h->xp_local, 0, sftm::kXpMailboxBytes);
-  if (e == cudaSuccess) e = cudaMalloc(&h->xp_err, sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(h->xp_err, 0, sizeof(int));
+  if (int rc = alloc_mailbox(h, P, rank)) return rc;
   cudaIpcMemHandle_t ih;
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&ih, h->xp_local);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  const cudaError_t e = cudaIpcGetMemHandle(&ih, h->xp_local);
   if (e != cudaSuccess) return check_cuda(h, e, "sf_tm_vp_mailbox_create");
   std::memcpy(ipc_handle_out, &ih, SF_TM_IPC_HANDLE_BYTES);
-  h->xp_P = P;
-  h->xp_rank = rank;
-  h->xp_mail[rank] = h->xp_local;
   return SF_TM_OK;
 }
 
@@ -781,7 +822,7 @@ int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles) {
   if (!h) return SF_TM_CONFIG_ERROR;
   if (int rc = use_device(h)) return rc;
   if (!h->xp_local) return fail(h, SF_TM_CONFIG_ERROR, "sf_tm_vp_mailbox_create first");
-  if (h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "mailboxes already open");
+  if (h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "mailboxes already open (or wired as a local group)");
   if (!ipc_handles) return fail(h, SF_TM_CONFIG_ERROR, "ipc_handles is required");
   const uint8_t* hb = static_cast<const uint8_t*>(ipc_handles);
   for (int q = 0; q < h->xp_P; ++q) {
@@ -805,24 +846,22 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
                                 float* out_logp, float* out_entropy, void* stream) {
   if (!h) return SF_TM_CONFIG_ERROR;
   if (int rc = use_device(h)) return rc;
-  if (!h->xp_ready) return fail(h, SF_TM_CONFIG_ERROR, "peer mailboxes not open (sf_tm_vp_mailbox_open)");
+  if (int rc = vp_fused_check(h, logits_shard, dtype, T, Vp, ld, dlogits, ld_d)) return rc;
   if (int rc = check_rows(h, logits_shard, dtype, T, Vp, ld, targets)) return rc;
   if (int rc = check_loss_params(h, params)) return rc;
   if (vocab_start < 0) return fail(h, SF_TM_CONFIG_ERROR, "vocab_start must be >= 0");
   if (!out_metrics) return fail(h, SF_TM_CONFIG_ERROR, "out_metrics is required");
-  if (ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "ld_d must be >= Vp");
-  const int64_t es = dtype == SF_TM_BF16 ? 2 : 4;
-  if ((reinterpret_cast<uintptr_t>(logits_shard) | reinterpret_cast<uintptr_t>(dlogits)) % 16 ||
-      (ld * es) % 16 || (ld_d * es) % 16 || (Vp * es) % 16)
-    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows, widths and strides");
+  if (T > 0 && (!old_logp || !ref_logp || !adv_tok || !w_tok || !dlogits))
+    return fail(h, SF_TM_CONFIG_ERROR, "missing required pointer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  ++h->xp_epoch;  // every rank calls in the same order, so epochs agree
+  // Every argument check is above this line: a rank's launch epoch advances
+  // only for a call that launches (or, for T == 0, that every rank makes with
+  // the same T), so the peers' epochs stay in step.
+  ++h->xp_epoch;
   if (T == 0) {
     return check_cuda(h, cudaMemsetAsync(out_metrics, 0, sizeof(float) * SF_TM_NUM_METRICS, s),
                       "sf_tm_vp_fused_loss_fwd_bwd");
   }
-  if (!old_logp || !ref_logp || !adv_tok || !w_tok || !dlogits)
-    return fail(h, SF_TM_CONFIG_ERROR, "missing required pointer");
   sftm::RowArgs a;
   a.logits = logits_shard;
   a.dtype = dtype;
@@ -845,7 +884,9 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
   a.xp_P = h->xp_P;
   a.xp_rank = h->xp_rank;
   a.xp_epoch = h->xp_epoch;
-  a.xp_err = h->xp_err;
+  a.xp_err = h->xp_err_d;
+  a.xp_abort = h->xp_abort;
+  a.xp_grid = h->xp_grid;
   static const unsigned long long timeout_ns = [] {
     const char* v = getenv("SF_TM_XP_TIMEOUT_S");
     const double sec = v ? atof(v) : 300.0;
@@ -857,10 +898,38 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
   a.max_partial_blocks = h->max_partial_blocks;
   sftm::LaunchInfo info;
   const int e = sftm::launch_loss_xp(a, s, &info);
-  if (e == -2) return fail(h, SF_TM_CONFIG_ERROR, "shard row too wide for the fused vocab-parallel kernel");
+  if (e == -2) return fail(h, SF_TM_INTERNAL, "fused vocab-parallel eligibility changed after the check");
   h->launches += static_cast<uint64_t>(info.launches);
   if (info.launches) h->last = info;
   return check_cuda(h, e, "sf_tm_vp_fused_loss_fwd_bwd");
+}
+
+int sf_tm_vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp, int64_t ld,
+                         const void* dlogits, int64_t ld_d) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  return vp_fused_check(h, logits_shard, dtype, T, Vp, ld, dlogits, ld_d);
+}
+
+int sf_tm_debug_vp_local_group(sf_tm_t* handles, int32_t P, int32_t grid_per_rank) {
+  if (!handles || P < 1 || P > sftm::kXpMaxP || grid_per_rank < 0) return SF_TM_CONFIG_ERROR;
+  for (int r = 0; r < P; ++r) {
+    sf_tm_t h = handles[r];
+    if (!h || h->device != handles[0]->device) return SF_TM_CONFIG_ERROR;
+    if (h->xp_local) return fail(h, SF_TM_CONFIG_ERROR, "mailbox already created on this handle");
+  }
+  for (int r = 0; r < P; ++r) {
+    if (int rc = use_device(handles[r])) return rc;
+    if (int rc = alloc_mailbox(handles[r], P, r)) return rc;
+  }
+  for (int r = 0; r < P; ++r) {
+    sf_tm_t h = handles[r];
+    for (int q = 0; q < P; ++q) h->xp_mail[q] = handles[q]->xp_local;
+    h->xp_grid = grid_per_rank;
+    h->xp_local_group = true;
+    h->xp_ready = true;
+  }
+  return SF_TM_OK;
 }
 
 int sf_tm_synth_logits(sf_tm_t h, void* logits, int32_t dtype, int64_t T, int64_t V, int64_t ld,

@@ -267,30 +267,25 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^a for a pair on the FMA pipe (no MUFU): round-to-nearest split a = j + f
-// with the 1.5 * 2^23 shifter, 2^f on [-0.5, 0.5] by a degree-3 polynomial
-// (max rel. error 1.0e-4, enough for bf16 outputs), exponent added as integer
-// (the shifter's low mantissa bits are j, so (bits << 23) == j << 23).
-// a is clamped to >= -127, where the result is exactly 0 (like the .ftz MUFU).
-__device__ __forceinline__ float2 ex2_poly2(float2 a) {
-  const float kShift = 12582912.f;
-  a.x = fmaxf(a.x, -127.f);
-  a.y = fmaxf(a.y, -127.f);
-  const float2 r = __fadd2_rn(a, make_float2(kShift, kShift));
-  const float2 jf = __fadd2_rn(r, make_float2(-kShift, -kShift));
-  const float2 f = __fadd2_rn(a, make_float2(-jf.x, -jf.y));
-  float2 q = __ffma2_rn(make_float2(0.05500892549753189f, 0.05500892549753189f), f,
-                        make_float2(0.2422109991312027f, 0.2422109991312027f));
-  q = __ffma2_rn(q, f, make_float2(0.6932829022407532f, 0.6932829022407532f));
-  q = __ffma2_rn(q, f, make_float2(1.f, 1.f));
-  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(r.x) << 23)),
-                     __int_as_float(__float_as_int(q.y) + (__float_as_int(r.y) << 23)));
-}
-
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 __device__ __forceinline__ float bf16_to_f32(uint16_t u) {
   return __uint_as_float(static_cast<uint32_t>(u) << 16);
+}
+
+// fp16x2 pack (round to nearest) and unpack: the row store of the e-store
+// loss kernel keeps 2^(z*log2e - base) as fp16 (11 significant bits).
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f16x2(uint32_t u) {
+  float lo, hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(u));
+  return make_float2(lo, hi);
 }
 
 // Round-to-nearest-even pack of two fp32 into bf16x2 (lo in the low half).

@@ -47,8 +47,10 @@ struct RowArgs {
   void* xp_mail[8] = {};
   int xp_rank = 0, xp_P = 0;
   unsigned long long xp_epoch = 0;  // launch sequence number, identical on all ranks
-  int* xp_err = nullptr;            // set to 1 before trapping on an exchange timeout
+  int* xp_err = nullptr;    // host-mapped: set to 1 when a launch gave up waiting for a peer
+  int* xp_abort = nullptr;  // device: first CTA to time out tells the others to stop waiting
   unsigned long long xp_timeout_ns = 300000000000ull;  // SF_TM_XP_TIMEOUT_S (default 300 s)
+  int xp_grid = 0;          // > 0: cap the exchange grid (emulated ranks sharing one GPU)
   // optional wait-time instrumentation (debug only): per-role clock64 sums
   unsigned long long* dbg = nullptr;
   // workspace (owned by the handle)
@@ -103,6 +105,9 @@ int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, La
 // Fused vocab-parallel loss (one CTA per SM, peer-mailbox exchange); -2 if the
 // shard is not eligible (then the caller reports a config error).
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info);
+// Whether a shard row of Vp elements fits one CTA's row store (the fused
+// vocab-parallel kernel runs one CTA per row per rank).
+bool loss_xp_eligible(int dtype, int64_t Vp);
 // Forward-only streaming pass (kModeFwd / kModeVpStats) on 16-B aligned rows (tm_fwd.cu).
 int launch_fwd_stream(const RowArgs& a, int mode, cudaStream_t s, LaunchInfo* info);
 

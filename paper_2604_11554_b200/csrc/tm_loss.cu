@@ -99,6 +99,11 @@ struct RowScal {
   uint32_t town;   // (thread owning the target << 8) | its element index j
 };
 constexpr int kMaxChunks = kStore - 2;      // a whole row slice must fit the row store
+// E-store (ES) rows: a chunk whose exponentials sum past this (relative to the
+// warp's current base) moves the base up, so every stored e = 2^(z*log2e -
+// base) is <= 2^11 and the fp16 row-store words cannot overflow; the values
+// that matter for p (>= 2^-18 of the row maximum) stay >= 2^-18 in fp16.
+constexpr float kEsMax = 2048.f;
 
 template <typename T>
 struct Geo {
@@ -226,7 +231,7 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // the boundary dlogits vectors are stored per element. Reads extend to whole
 // 16-B sectors inside the tensor; the very last row's tail sector is filled by
 // the producer with element loads instead, so nothing past the tensor is read.
-template <typename T, int C, bool XP = false, bool UA = false>
+template <typename T, int C, bool XP = false, bool UA = false, bool ES = false>
 __global__ void __launch_bounds__(kThreads, 1)
     loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
@@ -250,6 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t rcv_done[kCredD];  // XP: receiver progress (sender credit)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t sink_sh[kBW];
+  // ES: exponent base of each row-store slot's chunk, per forward warp, indexed
+  // by the slot's use parity (the next write of an entry is two uses later)
+  __shared__ float cbase[ES ? 2 : 1][ES ? kStore : 1][kFW];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -421,11 +429,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t ts0 = ts;
+      const uint32_t tph0 = tph;
+      bool nobase = false;  // ES: this warp's share of chunk 0 held nothing finite
+      (void)tph0;
       // One chunk: smem -> registers (slot released at once) -> TMEM stash ->
       // online softmax. `first` sets the exponent base from this thread's max of
       // chunk 0; `partial` masks elements past the slice end. Both are constants
       // at every call site, so the hot loop carries no per-chunk branches.
-      auto chunk = [&](int k, bool first, bool partial) {
+      auto chunk_raw = [&](int k, bool first, bool partial) {
         DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
         const uint32_t sa = ring_t + slot * kCB;
         uint4 v0 = lds128(sa);
@@ -533,6 +544,148 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
       };
+
+      // ES (e-store) chunk: the row store receives e = 2^(z*log2e - base) instead
+      // of the raw logits, so the backward forms p * |c0| with one multiply by
+      // 2^(base - lse2f) per chunk instead of one exponential per element. The
+      // base is warp-uniform (the warp's maximum of chunk 0), moved up when a
+      // chunk's exponentials sum past kEsMax; each slot's base goes to cbase.
+      // bf16 rows store e as fp16 (11 significant bits: the bf16 dlogits stay
+      // within 1 ulp), fp32 rows store fp32 e.
+      auto chunk_es = [&](int k, bool first, bool partial) {
+        DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
+        const uint32_t sa = ring_t + slot * kCB;
+        const uint4 v0 = lds128(sa);
+        const uint4 v1 = lds128(sa + kCB / 2);
+        const int rem = span - k * CE;             // valid elements end here (chunk coordinates)
+        const int lo = (UA && k == 0) ? mis : 0;   // ... and start here
+        // the warp's maximum of this chunk's valid elements (x * c)
+        auto chunk_max = [&]() {
+          float x[NE];
+          unpack(logits, v0, v1, x);
+          float xm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            const int pj = elem_off<T>(ftid, j);
+            if (!partial || (pj >= lo && pj < rem)) xm = fmaxf(xm, x[j]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+          return xm * c;
+        };
+        if (first) {
+          m2 = chunk_max();
+          if (!(m2 > -INFINITY)) {  // nothing finite: provisional base, repaired at row end
+            m2 = 0.f;
+            nobase = true;
+          }
+        }
+        // exponentials of the chunk against the current base, straight into the
+        // row-store words (invalid positions 0) and the chunk's partial sums
+        uint32_t q[8];
+        float2 cs[2], cw[2];
+        auto expo = [&]() {
+          float x[NE];
+          unpack(logits, v0, v1, x);
+          cs[0] = cs[1] = cw[0] = cw[1] = make_float2(0.f, 0.f);
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p0 = v * G::HALF + EV * ftid;
+            const bool whole = !partial || (p0 >= lo && p0 + EV <= rem);
+            float ev[EV];
+            if (whole) {
+#pragma unroll
+              for (int h = 0; h < EV / 2; ++h) {
+                const int p = v * (EV / 2) + h;
+                const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
+                const float2 e2 = make_float2(ex2(av.x), ex2(av.y));
+                cs[h & 1] = __fadd2_rn(cs[h & 1], e2);
+                cw[h & 1] = __ffma2_rn(e2, av, cw[h & 1]);
+                ev[2 * h] = e2.x;
+                ev[2 * h + 1] = e2.y;
+              }
+            } else {
+              // boundary vector of an unaligned row (element masks), or a vector
+              // past the end of an aligned slice (all masked)
+#pragma unroll
+              for (int j = 0; j < EV; ++j) {
+                const int pj = p0 + j;
+                ev[j] = 0.f;
+                if (UA && pj >= lo && pj < rem && x[v * EV + j] != -INFINITY) {
+                  const float av = fmaf(x[v * EV + j], c, -m2);
+                  ev[j] = ex2(av);
+                  cs[0].x += ev[j];
+                  cw[0].x = fmaf(ev[j], av, cw[0].x);
+                }
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              if constexpr (sizeof(T) == 2) {
+                q[4 * v + h] = pack_f16x2(ev[2 * h], ev[2 * h + 1]);
+              } else {
+                q[4 * v + h] = __float_as_uint(ev[h]);
+              }
+            }
+          }
+        };
+        expo();
+        {
+          const float2 c01 = __fadd2_rn(cs[0], cs[1]);
+          if (__any_sync(0xffffffffu, !(c01.x + c01.y <= kEsMax))) {
+            // rare: this chunk rises far above the base. New base = the warp's
+            // maximum of this chunk; rescale the running sums, redo the chunk.
+            const float nb = fmaxf(m2, chunk_max());
+            const float d = m2 - nb, f = ex2(d);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              w2[i] = make_float2(f * fmaf(s2[i].x, d, w2[i].x), f * fmaf(s2[i].y, d, w2[i].y));
+              s2[i] = make_float2(s2[i].x * f, s2[i].y * f);
+            }
+            m2 = nb;
+            expo();
+          }
+        }
+        s2[0] = __fadd2_rn(s2[0], cs[0]);
+        s2[1] = __fadd2_rn(s2[1], cs[1]);
+        w2[0] = __fadd2_rn(w2[0], cw[0]);
+        w2[1] = __fadd2_rn(w2[1], cw[1]);
+        uint4 q0 = make_uint4(q[0], q[1], q[2], q[3]), q1 = make_uint4(q[4], q[5], q[6], q[7]);
+        DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
+        const bool in_tmem = ts < kTSlots;
+        if (in_tmem) {
+          tc_fence_after();
+          tmem_st8(tm_t + ts * static_cast<uint32_t>(kSlotCols), q0, q1);
+        } else {
+          const uint32_t sa2 = stash_t + (ts - kTSlots) * kCB;
+          sts128(sa2, q0);
+          sts128(sa2 + kCB / 2, q1);
+        }
+        // the row-store words were computed from v0/v1: both LDS have returned
+        mbar_arrive(empty0 + 8u * slot);
+        if (++slot == kSlots) {
+          slot = 0;
+          ph ^= 1u;
+        }
+        if (lane == 0) cbase[tph & (ES ? 1u : 0u)][ES ? ts : 0][fw] = m2;
+        if (in_tmem) {
+          tmem_wait_st(q0, q1);
+          tc_fence_before();
+        }
+        mbar_arrive(tfull0 + 8u * ts);  // release: orders the smem stores (and cbase) too
+        if (++ts == kStore) {
+          ts = 0;
+          tph ^= 1u;
+        }
+      };
+      auto chunk = [&](int k, bool first, bool partial) {
+        if constexpr (ES) {
+          chunk_es(k, first, partial);
+        } else {
+          chunk_raw(k, first, partial);
+        }
+      };
       if constexpr (UA) {
         // peeled like the aligned schedule: only the front and tail chunks are masked
         const int nfull_r = span / CE;
@@ -558,6 +711,77 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
       // (a logit > 126/log2e above the chunk-0 base) made s or w non-finite:
       // recompute this thread's partials exactly from its TMEM words.
+      if constexpr (ES) {
+        // Repair (rare): a -inf logit (0 * -inf in w) or a warp share whose
+        // chunk 0 held nothing finite. The row store holds exponentials, not
+        // logits: re-read this warp's elements of the row from HBM (the row's
+        // dlogits are not written yet, so in-place rows are intact), rebase on
+        // the warp's true maximum and rewrite the row store and its bases.
+        const bool bad_es = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f) || nobase;
+        if (__any_sync(0xffffffffu, bad_es)) {
+          const T* rowg = logits + t * a.ld + slice_start - mis;
+          float mx = -INFINITY;
+          for (int k = 0; k < nck_r; ++k) {
+            const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+#pragma unroll
+            for (int j = 0; j < NE; ++j) {
+              const int pj = elem_off<T>(ftid, j);
+              if (pj >= lo && pj < rem) mx = fmaxf(mx, ldg_elem(rowg, static_cast<int64_t>(k) * CE + pj));
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          const float mb2 = (mx > -INFINITY) ? mx * c : 0.f;
+          float sr = 0.f, wr = 0.f;
+          uint32_t q = ts0, qp = tph0;
+          for (int k = 0; k < nck_r; ++k) {
+            const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+            float e[NE];
+#pragma unroll
+            for (int j = 0; j < NE; ++j) {
+              const int pj = elem_off<T>(ftid, j);
+              e[j] = 0.f;
+              if (pj >= lo && pj < rem) {
+                const float xv = ldg_elem(rowg, static_cast<int64_t>(k) * CE + pj);
+                if (xv != -INFINITY) {
+                  const float av = fmaf(xv, c, -mb2);
+                  e[j] = ex2(av);
+                  sr += e[j];
+                  wr = fmaf(e[j], av, wr);
+                }
+              }
+            }
+            uint4 q0, q1;
+            if constexpr (sizeof(T) == 2) {
+              q0 = make_uint4(pack_f16x2(e[0], e[1]), pack_f16x2(e[2], e[3]), pack_f16x2(e[4], e[5]),
+                              pack_f16x2(e[6], e[7]));
+              q1 = make_uint4(pack_f16x2(e[8], e[9]), pack_f16x2(e[10], e[11]), pack_f16x2(e[12], e[13]),
+                              pack_f16x2(e[14], e[15]));
+            } else {
+              q0 = make_uint4(__float_as_uint(e[0]), __float_as_uint(e[1]), __float_as_uint(e[2]),
+                              __float_as_uint(e[3]));
+              q1 = make_uint4(__float_as_uint(e[4]), __float_as_uint(e[5]), __float_as_uint(e[6]),
+                              __float_as_uint(e[7]));
+            }
+            if (q < static_cast<uint32_t>(kTSlots)) {
+              tmem_st8(tm_t + q * static_cast<uint32_t>(kSlotCols), q0, q1);
+            } else {
+              sts128(stash_t + (q - kTSlots) * kCB, q0);
+              sts128(stash_t + (q - kTSlots) * kCB + kCB / 2, q1);
+            }
+            if (lane == 0) cbase[qp & (ES ? 1u : 0u)][ES ? q : 0][fw] = mb2;
+            if (++q == kStore) {
+              q = 0;
+              qp ^= 1u;
+            }
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __threadfence_block();  // order every lane's rewrite before lane 0's release below
+          __syncwarp();
+          my = Stats{mb2, sr, wr};
+        }
+      } else {
       const bool bad = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f);
       if (__any_sync(0xffffffffu, bad)) {
         float mx = -INFINITY;
@@ -598,6 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (bad) my = Stats{mb2, sr, wr};
       }
+      }  // ES / raw repair
       if (my.s == 0.f) my = stats_empty();  // nothing finite in this thread's share
       // Per-warp partial -> smem ring; no CTA barrier: the control warp
       // merges the 12 partials, so forward warps go straight to the next row.
@@ -706,9 +931,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t t0 = globaltimer_ns();
               do {
                 __nanosleep(64);
-                if (globaltimer_ns() - t0 > a.xp_timeout_ns) {  // a peer never launched
-                  if (a.xp_err) atomicExch(a.xp_err, 1);
-                  __trap();
+                // A peer that never launches (or died) must not hang the
+                // context: past the timeout (or once another CTA of this launch
+                // gave up) stop waiting, flag the launch as failed (host-mapped
+                // word, surfaced by the next API call as Internal) and let the
+                // kernel run to completion on the stale mailbox values.
+                const uint64_t el = globaltimer_ns() - t0;
+                if (el > 1000000ull &&
+                    (el > a.xp_timeout_ns || *reinterpret_cast<volatile int*>(a.xp_abort) != 0)) {
+                  atomicExch(a.xp_abort, 1);
+                  *reinterpret_cast<volatile int*>(a.xp_err) = 1;
+                  __threadfence_system();
+                  break;
                 }
                 ld_sys_v2u64(&src->w[0], q0, q1);
                 ld_sys_v2u64(&src->w[2], q2, q3);
@@ -985,17 +1219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int p = 0; p < NE / 2; ++p) {
             if ((2 * p < EV) ? vok0 : vok1) {
               const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nl2);
-#ifdef SFTM_POLY_EXP
-              if (p < SFTM_POLY_EXP) {  // A/B: this pair's exponentials on the FMA pipe
-                const float2 e2 = ex2_poly2(av);
-                gr[2 * p] = e2.x;
-                gr[2 * p + 1] = e2.y;
-              } else
-#endif
-              {
-                gr[2 * p] = ex2(av.x);
-                gr[2 * p + 1] = ex2(av.y);
-              }
+              gr[2 * p] = ex2(av.x);
+              gr[2 * p + 1] = ex2(av.y);
             } else {
               gr[2 * p] = gr[2 * p + 1] = 0.f;
             }
@@ -1109,8 +1334,105 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (late) mbar_arrive(rel);
       };
+      // ES chunk: e = 2^(z*log2e - base) from the row store (fp16 for bf16 rows,
+      // fp32 for fp32 rows); dlogits = gt*[v == y] - c0*p = e * f (+ gt), with
+      // f = -sign(c0) * 2^(base - lse2f) once per chunk (lse2f folds log2|c0|).
+      auto bchunk_es = [&](int k, bool partial) {
+        DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
+        tc_fence_after();
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
+        // this slot's base: the forward rewrites this entry two uses of the slot
+        // later, so reading it here cannot race the early TMEM-slot release
+        const float base = cbase[tph & (ES ? 1u : 0u)][ES ? ts : 0][bw];
+        const uint32_t rel = tempty0 + 8u * ts;
+        const bool late = ts >= kTSlots;
+        if (!late) {
+          tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
+          tmem_wait_ld(w0, w1);
+          tc_fence_before();
+          mbar_arrive(rel);
+        } else {
+          w0 = lds128(stash_t + (ts - kTSlots) * kCB);
+          w1 = lds128(stash_t + (ts - kTSlots) * kCB + kCB / 2);
+        }
+        if (++ts == kStore) {
+          ts = 0;
+          tph ^= 1u;
+        }
+        const float fm = ex2(base - lse2f);
+        const float f = neg ? -fm : fm;
+        const float2 f2 = make_float2(f, f);
+        float gr[NE];
+        if constexpr (sizeof(T) == 2) {
+          const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const float2 g2 = __fmul2_rn(unpack_f16x2(wd[p]), f2);
+            gr[2 * p] = g2.x;
+            gr[2 * p + 1] = g2.y;
+          }
+        } else {
+          const float2 g0 = __fmul2_rn(make_float2(__uint_as_float(w0.x), __uint_as_float(w0.y)), f2);
+          const float2 g1 = __fmul2_rn(make_float2(__uint_as_float(w0.z), __uint_as_float(w0.w)), f2);
+          const float2 g2 = __fmul2_rn(make_float2(__uint_as_float(w1.x), __uint_as_float(w1.y)), f2);
+          const float2 g3 = __fmul2_rn(make_float2(__uint_as_float(w1.z), __uint_as_float(w1.w)), f2);
+          gr[0] = g0.x; gr[1] = g0.y; gr[2] = g1.x; gr[3] = g1.y;
+          gr[4] = g2.x; gr[5] = g2.y; gr[6] = g3.x; gr[7] = g3.y;
+        }
+        if (k == ck) {
+#pragma unroll
+          for (int j = 0; j < NE; ++j)
+            if (j == jt) gr[j] += gt;
+        }
+        T* dst = drow + k * CE;
+        const int rem = span - k * CE;
+        const uint32_t dep = w0.x ^ w1.w ^ __float_as_uint(f);
+        if (!partial) {
+          store_vec(dst + EV * btid, gr);
+          store_vec(dst + G::HALF + EV * btid, gr + EV);
+        } else if (UA) {
+          const int lo = (k == 0) ? mis : 0;
+          bool any = false;
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p0 = v * G::HALF + EV * btid;
+            if (p0 >= lo && p0 + EV <= rem) {
+              store_vec(dst + p0, gr + v * EV);
+              any = true;
+            } else {
+#pragma unroll
+              for (int j = 0; j < EV; ++j)
+                if (p0 + j >= lo && p0 + j < rem) {
+                  st1(dst + p0 + j, gr[v * EV + j]);
+                  any = true;
+                }
+            }
+          }
+          if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
+        } else {
+          // vector-granular tail; a thread storing nothing still orders its
+          // loads before the release through a dependent (dummy) smem store
+          const bool s0 = EV * btid < rem;
+          if (s0) store_vec(dst + EV * btid, gr);
+          if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
+          if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
+        }
+        if (late) mbar_arrive(rel);
+      };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
-      if constexpr (UA) {
+      if constexpr (ES) {
+        const int nfull_r = UA ? span / CE : nfull;
+        const bool front = UA && (mis > 0 || span < CE);
+        if (nck_r > 0) {
+          if (front || nfull_r == 0) {
+            bchunk_es(0, true);
+          } else {
+            bchunk_es(0, false);
+          }
+          for (int k = 1; k < nfull_r; ++k) bchunk_es(k, false);
+          if (nck_r > nfull_r && nck_r > 1) bchunk_es(nck_r - 1, true);
+        }
+      } else if constexpr (UA) {
         const int nfull_r = span / CE;
         const bool front = mis > 0 || span < CE;
         auto sched = [&](auto md) {
@@ -1167,9 +1489,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
-template <typename T, int C, bool XP = false, bool UA = false>
+template <typename T, int C, bool XP = false, bool UA = false, bool ES = false>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  auto kern = loss_tmem_kernel<T, C, XP, UA>;
+  auto kern = loss_tmem_kernel<T, C, XP, UA, ES>;
   static PerDevice cache;  // per instantiation and device
   int& max_active = cache();
   {
@@ -1205,7 +1527,10 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
     }
   }
   int64_t ncl = a.T < max_active ? a.T : max_active;
-  if (XP) ncl = max_active < kXpMaxCtas ? max_active : kXpMaxCtas;  // same grid on every rank, whatever T
+  if (XP) {  // same grid on every rank, whatever T
+    ncl = max_active < kXpMaxCtas ? max_active : kXpMaxCtas;
+    if (a.xp_grid > 0 && a.xp_grid < ncl) ncl = a.xp_grid;  // co-resident emulated ranks (tests)
+  }
   RowArgs ad = a;
   ad.dbg = debug_counters();
   if (ncl > a.max_partial_blocks) ncl = a.max_partial_blocks;
@@ -1236,19 +1561,35 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   return e;
 }
 
+// The e-store schedule takes every row whose gradient has no entropy term
+// (entropy_coef == 0, the DAPO default): the backward then needs p*c0 only.
+// SFTM_ES=0 selects the raw-logit row store for A/B runs.
+inline bool use_es(const RowArgs& a) {
+  static const bool off = [] {
+    const char* v = getenv("SFTM_ES");
+    return v && v[0] == '0';
+  }();
+  return !off && a.ent_coef == 0.f;
+}
+
+template <typename T, bool ES>
+int launch_with_es(const RowArgs& a, int C, int64_t slice, cudaStream_t s, LaunchInfo* info) {
+  switch (C) {
+    case 1: return launch_c<T, 1, false, false, ES>(a, slice, s, info);
+    case 2: return launch_c<T, 2, false, false, ES>(a, slice, s, info);
+    case 3: return launch_c<T, 3, false, false, ES>(a, slice, s, info);
+    case 4: return launch_c<T, 4, false, false, ES>(a, slice, s, info);
+    case 8: return launch_c<T, 8, false, false, ES>(a, slice, s, info);
+  }
+  return -2;
+}
+
 template <typename T>
 int launch_with(const RowArgs& a, int C, cudaStream_t s, LaunchInfo* info) {
   using G = Geo<T>;
   int64_t slice = (a.V + C - 1) / C;
   slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
-  switch (C) {
-    case 1: return launch_c<T, 1>(a, slice, s, info);
-    case 2: return launch_c<T, 2>(a, slice, s, info);
-    case 3: return launch_c<T, 3>(a, slice, s, info);
-    case 4: return launch_c<T, 4>(a, slice, s, info);
-    case 8: return launch_c<T, 8>(a, slice, s, info);
-  }
-  return -2;
+  return use_es(a) ? launch_with_es<T, true>(a, C, slice, s, info) : launch_with_es<T, false>(a, C, slice, s, info);
 }
 
 template <typename T>
@@ -1264,7 +1605,8 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
   if (ua) {
     if ((a.V + G::EV - 1 + G::CE - 1) / G::CE > kMaxChunks) return -2;
-    return launch_c<T, 1, false, true>(a, a.V, s, info);
+    return use_es(a) ? launch_c<T, 1, false, true, true>(a, a.V, s, info)
+                     : launch_c<T, 1, false, true, false>(a, a.V, s, info);
   }
   static const int forced = [] {  // tuning knob: SFTM_LOSS_C=1|2|3|4|8
     const char* v = getenv("SFTM_LOSS_C");
@@ -1287,6 +1629,15 @@ int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   return loss::launch_t<float>(a, s, info);
 }
 
+bool loss_xp_eligible(int dtype, int64_t Vp) {
+  auto fits = [&](auto tag) {
+    using G = loss::Geo<decltype(tag)>;
+    const int64_t slice = (Vp + G::EV - 1) / G::EV * G::EV;
+    return (slice + G::CE - 1) / G::CE <= loss::kMaxChunks;
+  };
+  return dtype == 1 ? fits(uint16_t{}) : fits(float{});
+}
+
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   // one CTA per row per rank: the whole shard row slice must fit the row store
   auto go = [&](auto tag) -> int {
@@ -1294,7 +1645,8 @@ int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
     using G = loss::Geo<T>;
     int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
     if ((slice + G::CE - 1) / G::CE > loss::kMaxChunks) return -2;
-    return loss::launch_c<T, 1, true>(a, slice, s, info);
+    return loss::use_es(a) ? loss::launch_c<T, 1, true, false, true>(a, slice, s, info)
+                           : loss::launch_c<T, 1, true, false, false>(a, slice, s, info);
   };
   if (a.dtype == 1) return go(uint16_t{});
   return go(float{});

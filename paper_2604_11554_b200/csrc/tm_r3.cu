@@ -687,7 +687,7 @@ int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E
   const int64_t rows = L * T;
   const bool al = (reinterpret_cast<uintptr_t>(w) % 16 == 0) && (reinterpret_cast<uintptr_t>(dw) % 16 == 0) &&
                   (reinterpret_cast<uintptr_t>(rec_idx) % (idx_dtype == 1 ? 4 : 16) == 0);
-  if (renorm && k == 8 && E % 64 == 0 && E <= 256 && al && !getenv("SFTM_R3_BWD_OLD")) {
+  if (renorm && k == 8 && E % 64 == 0 && E <= 256 && al) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

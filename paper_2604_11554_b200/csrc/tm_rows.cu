@@ -9,7 +9,7 @@
 //   fwd_stream_kernel (tm_fwd.cu)  — forward only (kModeFwd, kModeVpStats).
 //   rows_ring_kernel   — a TMA-ring streaming kernel with 16 compute warps: the
 //                        two-pass vocab-parallel shard backward (kModeVpBwd), and
-//                        the A/B baseline for the forward modes (SFTM_FWD_RING=1).
+//                        the forward modes when the streaming kernel cannot take them.
 //   rows_generic_kernel — fallback for what the above cannot take (dlogits at a
 //                        different 16-B phase than the logits, rows too wide
 //                        for any row store, unaligned rows in kModeVpBwd): two
@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -436,12 +437,11 @@ __global__ void __launch_bounds__(kGT) rows_generic_kernel(const RowArgs a) {
 // ===========================================================================
 // Host-side launch logic.
 // ===========================================================================
-int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info);  // tm_loss.cu (v2 schedule)
-int launch_loss_v3(const RowArgs& a, cudaStream_t s, LaunchInfo* info);    // tm_loss3.cu (v3 schedule)
+int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info);  // tm_loss.cu
 
 namespace {
 
-bool g_force_generic = false;
+std::atomic<bool> g_force_generic{false};
 std::mutex g_mu;
 
 struct DevInfo {
@@ -555,22 +555,11 @@ int dispatch(const RowArgs& a, int mode, cudaStream_t s, std::string* err, Launc
   const bool fwd_ok = !g_force_generic && (mode == kModeFwd || mode == kModeVpStats) && lb % es == 0;
   if (ring_ok || ua_ok || fwd_ok) {
     if (mode == kModeFwdBwd) {
-      // default: role-split schedule (tm_loss.cu); SFTM_LOSS_VARIANT=3 selects the
-      // per-warp software-pipelined schedule (tm_loss3.cu) for A/B comparisons
-      static const int variant = [] {
-        const char* v = getenv("SFTM_LOSS_VARIANT");
-        return (v && v[0] == '3') ? 3 : 2;
-      }();
-      const int e = (variant == 2 || !ring_ok) ? launch_loss_tmem(a, s, info) : launch_loss_v3(a, s, info);
+      const int e = launch_loss_tmem(a, s, info);
       if (e != -2) return e;  // -2: slice too wide for TMEM residency -> generic
     } else {
-      // forward-only modes: the 24-warp streaming kernel (tm_fwd.cu);
-      // SFTM_FWD_RING=1 selects the older 16-warp ring kernel for A/B runs
-      static const bool old_ring = [] {
-        const char* v = getenv("SFTM_FWD_RING");
-        return v && v[0] == '1';
-      }();
-      if (!old_ring && (mode == kModeFwd || mode == kModeVpStats)) {
+      // forward-only modes: the 24-warp streaming kernel (tm_fwd.cu)
+      if (mode == kModeFwd || mode == kModeVpStats) {
         const int e = launch_fwd_stream(a, mode, s, info);
         if (e != -2) return e;
       }

@@ -61,7 +61,7 @@ class Handle:
         k, c, g = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         self.check(_lib.lib().sf_tm_last_launch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(g)),
                    "sf_tm_last_launch")
-        names = {0: "rows_ring_kernel", 1: "rows_generic_kernel", 2: "loss_tmem_kernel", 3: "loss_v3_kernel",
+        names = {0: "rows_ring_kernel", 1: "rows_generic_kernel", 2: "loss_tmem_kernel",
                  4: "loss_tmem_kernel[peer-exchange]", 5: "fwd_stream_kernel"}
         return {"kernel": names.get(k.value, str(k.value)), "cluster": c.value, "grid": g.value}
 
@@ -308,11 +308,35 @@ def vp_mailbox_open(handles: list, device: Optional[int] = None):
     h.check(_lib.lib().sf_tm_vp_mailbox_open(h.ptr, buf), "sf_tm_vp_mailbox_open")
 
 
-def vp_fused_loss_fwd_bwd(shard, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
-                          params: Optional[LossParams] = None, dlogits=None, want_logp: bool = False, metrics=None):
-    """Single-pass vocab-parallel loss: the exchange happens inside the kernel."""
+def vp_fused_check(shard, dlogits=None) -> tuple[int, str]:
+    """sf_tm_vp_fused_check: (Errc, message) for this rank's shard, no side effect."""
     d = _dev(shard)
     h = handle(d)
+    dt, T, Vp, ld = _rows(shard)
+    ld_d = ld if dlogits is None else dlogits.stride(0)
+    ptr = _p(shard) if dlogits is None else _p(dlogits)
+    rc = _lib.lib().sf_tm_vp_fused_check(h.ptr, _p(shard), dt, T, Vp, ld, ptr, ld_d)
+    msg = _lib.lib().sf_tm_last_error(h.ptr) if rc else b""
+    return int(rc), (msg.decode() if msg else "")
+
+
+def vp_local_group(handles: list, grid_per_rank: int = 0):
+    """Wire P handles of one device into an in-process vocab-parallel group
+    (sf_tm_debug_vp_local_group): P ranks emulated on one GPU."""
+    arr = (_lib._H * len(handles))(*[hh.ptr.value for hh in handles])
+    rc = _lib.lib().sf_tm_debug_vp_local_group(arr, len(handles), grid_per_rank)
+    if rc != 0:
+        raise TrainMathError(rc, "sf_tm_debug_vp_local_group failed")
+
+
+def vp_fused_loss_fwd_bwd(shard, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
+                          params: Optional[LossParams] = None, dlogits=None, want_logp: bool = False, metrics=None,
+                          h: Optional[Handle] = None, stream=None):
+    """Single-pass vocab-parallel loss: the exchange happens inside the kernel.
+    `h`: the rank's Handle (default: the device's shared handle; emulated
+    in-process groups pass their own)."""
+    d = _dev(shard)
+    h = handle(d) if h is None else h
     dt, T, Vp, ld = _rows(shard)
     if params is None:
         params = default_loss_params()
@@ -325,7 +349,8 @@ def vp_fused_loss_fwd_bwd(shard, vocab_start: int, targets, old_logp, ref_logp, 
     rc = _lib.lib().sf_tm_vp_fused_loss_fwd_bwd(h.ptr, _p(shard), dt, T, Vp, ld, vocab_start, _p(targets),
                                                 _p(old_logp), _p(ref_logp), _p(adv_tok), _p(w_tok),
                                                 ctypes.byref(params), _p(dlogits), dlogits.stride(0), _p(metrics),
-                                                _p(logp), _p(ent), _stream(d))
+                                                _p(logp), _p(ent),
+                                                _stream(d) if stream is None else ctypes.c_void_p(stream.cuda_stream))
     h.check(rc, "sf_tm_vp_fused_loss_fwd_bwd")
     return metrics, dlogits, logp, ent
 

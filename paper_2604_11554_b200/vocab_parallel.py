@@ -70,26 +70,40 @@ def vp_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp,
                               dlogits=dlogits, want_logp=want_logp)
 
 
-_peer_groups: dict = {}
+_peer_groups: dict = {}   # (device, group's global ranks) -> agreed outcome
+_bound: dict = {}         # device -> group key its handle's mailbox is bound to
+
+
+def _group_key(group):
+    ranks = tuple(dist.get_process_group_ranks(group)) if group is not None else \
+        tuple(range(dist.get_world_size()))
+    return ranks
 
 
 def open_peer_exchange(group=None) -> bool:
     """Create this rank's peer mailbox, all-gather the 64-byte CUDA IPC handles
     over `group` (any backend) and map the peers. The outcome is agreed on by
     all ranks: if any rank cannot map its peers (no P2P path), every rank
-    reports False and the callers use the two-pass NCCL form. Idempotent per
-    device."""
+    reports False and the callers use the two-pass NCCL form. Cached per
+    (device, group); a handle's mailbox serves one group only, so a second
+    group on the same device gets False (two-pass) on every rank."""
     dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
-    if dev in _peer_groups:
-        return _peer_groups[dev]
+    key = (dev, _group_key(group))
+    if key in _peer_groups:
+        return _peer_groups[key]
     P = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ok = True
+    mine = None
+    if dev in _bound:
+        ok = False  # this device's handle is already bound to another group
+    else:
+        try:
+            mine = tm.vp_mailbox_create(P, rank, dev)
+            _bound[dev] = key
+        except tm.TrainMathError:
+            ok = False
     handles = [None] * P
-    try:
-        mine = tm.vp_mailbox_create(P, rank, dev)
-    except tm.TrainMathError:
-        mine, ok = None, False
     dist.all_gather_object(handles, mine, group=group)
     if ok and all(h is not None for h in handles):
         try:
@@ -100,8 +114,15 @@ def open_peer_exchange(group=None) -> bool:
         ok = False
     flags = [None] * P
     dist.all_gather_object(flags, ok, group=group)
-    _peer_groups[dev] = all(flags)
-    return _peer_groups[dev]
+    _peer_groups[key] = all(flags)
+    return _peer_groups[key]
+
+
+def _all_ok(ok: bool, device, group) -> bool:
+    """Agree on a per-rank flag (MIN over the group, one 4-byte all-reduce)."""
+    f = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
+    return bool(f.item())
 
 
 def vp_fused_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old_logp, ref_logp, adv_tok, w_tok,
@@ -109,8 +130,15 @@ def vp_fused_pg_loss_fwd_bwd(shard: torch.Tensor, vocab_start: int, targets, old
                              metrics=None):
     """Single-pass vocab-parallel fused loss (exchange inside the kernel over
     NVLink peer memory); same outputs as vp_pg_loss_fwd_bwd, which it falls back
-    to (on every rank) when the ranks cannot map each other's memory."""
-    if not open_peer_exchange(group):
+    to on every rank when the ranks cannot map each other's memory or when any
+    rank's shard is not eligible (shape, alignment, row-store size) -- the
+    eligibility is agreed before the kernel launches, so no rank is left
+    waiting for a peer that did not launch."""
+    use = open_peer_exchange(group)
+    if use:
+        rc, _ = tm.vp_fused_check(shard, dlogits)
+        use = _all_ok(rc == 0, shard.device, group)
+    if not use:
         met, dl, lp, ent = vp_pg_loss_fwd_bwd(shard, vocab_start, targets, old_logp, ref_logp, adv_tok, w_tok, params,
                                               dlogits=dlogits, group=group, want_logp=want_logp)
         if metrics is not None:

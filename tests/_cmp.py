@@ -66,3 +66,33 @@ def loss_row_scale(og, w, a, olp, old, ref, beta=0.0, kl_mode=0, ent=0.0, inv_ta
     dkl = {0: np.abs(1 - np.exp(np.minimum(d, 80))), 1: np.ones_like(d), 2: np.abs(d), 3: np.ones_like(d)}[kl_mode]
     terms = np.abs(np.asarray(a, np.float64)) * ratio + abs(beta) * dkl
     return (np.abs(og) + w * terms + w * abs(ent) * 60.0) * inv_tau
+
+
+def metrics_from_rows(logp, ent, old, ref, adv, w, eps_lo=0.2, eps_hi=0.28, dual_c=0.0, beta=0.0, ent_coef=0.0,
+                      kl_mode=0):
+    """The step metrics [loss, pg, kl, entropy, clipfrac, ratio, n_active, ppo_kl]
+    as fp64 sums over rows, from per-row logp / entropy: a numpy restatement of
+    the per-row terms of orc_pg_loss_fwd_bwd (oracle/sf_oracle.c), pinned
+    against it in tests/test_oracle.py. Lets a full-size GPU run check its
+    reduction from its own per-row outputs when the oracle cannot hold every
+    row."""
+    f = lambda a: np.asarray(a, np.float64)
+    lp, H, o, r, A, w = f(logp), f(ent), f(old), f(ref), f(adv), f(w)
+    act = w != 0
+    lp, H, o, r, A, w = lp[act], H[act], o[act], r[act], A[act], w[act]
+    ratio = np.exp(lp - o)
+    clip_hi = (A > 0) & (ratio > 1 + eps_hi)
+    clip_lo = (A < 0) & (ratio < 1 - eps_lo)
+    rc = np.clip(ratio, 1 - eps_lo, 1 + eps_hi)
+    pg = np.maximum(-ratio * A, -rc * A)
+    clipped = clip_hi | clip_lo
+    if dual_c > 1:
+        cap = -dual_c * A
+        dc = (A < 0) & (pg > cap)
+        pg = np.where(dc, cap, pg)
+        clipped |= dc
+    d = r - lp
+    kl = {0: np.exp(d) - d - 1, 1: -d, 2: 0.5 * d * d, 3: np.abs(d)}[kl_mode]
+    loss = pg + (beta * kl if beta != 0 else 0.0) - ent_coef * H
+    return np.array([(w * loss).sum(), (w * pg).sum(), (w * kl).sum(), (w * H).sum(), (w * clipped).sum(),
+                     (w * ratio).sum(), float(act.sum()), (w * (o - lp)).sum()])

@@ -4,6 +4,10 @@ import sys
 
 import pytest
 
+# a fused vocab-parallel launch whose peers never arrive gives up after this
+# long (tests/test_gpu_configs.py exercises it); read once per process
+os.environ.setdefault("SF_TM_XP_TIMEOUT_S", "10")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -27,6 +27,11 @@ def _worker(rank, world, port, q):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
@@ -45,14 +50,29 @@ def _worker(rank, world, port, q):
         w = (torch.rand(T, generator=g) < 0.9).float().to(dev) / T
         met_f, dl_f, lp_f, ent_f = tm.pg_loss_fwd_bwd(logits, targets, old, ref, adv, w, want_logp=True)
         b = shard_bounds(V, world)
+        # the fp64 oracle on the same rows: every dlogits entry of this rank's
+        # shard within 1 bf16 ulp (+ the target-entry floor), near-clip rows aside
+        from oracle import oracle as orc
+        from tests._cmp import bf16_ulp, near_clip_rows
+
+        orc.lib()
+        bits = logits.view(torch.int16).cpu().numpy().view(np.uint16)
+        o_np, r_np, a_np, w_np = (x.cpu().numpy() for x in (old, ref, adv, w))
+        _, odl, olp, _, og = orc.pg_loss_fwd_bwd(bits, targets.cpu().numpy(), o_np, r_np, a_np, w_np)
+        near = near_clip_rows(olp, o_np, a_np, 0.2, 0.28)
+        odl_sh = odl[:, b[rank]:b[rank + 1]]
+        lim_sh = bf16_ulp(odl_sh) + 4e-6 * np.abs(og)[:, None] + 1e-30
+
+        def grad_ok(d):
+            got = orc.bf16_bits_to_f32(d.view(torch.int16).cpu().numpy().view(np.uint16)).astype(np.float64)
+            return bool(((np.abs(got - odl_sh) <= lim_sh) | near[:, None]).all())
+
         shard = logits[:, b[rank]:b[rank + 1]].contiguous()
         met, dsh, lpv, entv = vp_pg_loss_fwd_bwd(shard, b[rank], targets, old, ref, adv, w, want_logp=True)
         torch.cuda.synchronize()
         ok_lp = torch.allclose(lpv, lp_f, atol=2e-6, rtol=2e-6)
         ok_ent = torch.allclose(entv, ent_f, atol=2e-5, rtol=2e-5)
-        ref_sh = dl_f[:, b[rank]:b[rank + 1]].float()
-        diff = (dsh.float() - ref_sh).abs()
-        ok_dl = bool((diff <= ref_sh.abs() * 2 ** -7 + 1e-7).float().mean() > 0.9999)
+        ok_dl = grad_ok(dsh)
         allm = [torch.empty_like(met) for _ in range(world)]
         dist.all_gather(allm, met)
         ok_same = all(torch.equal(m, allm[0]) for m in allm)
@@ -63,12 +83,11 @@ def _worker(rank, world, port, q):
         for it in range(3):
             mx, dx, lpx, entx = vp_fused_pg_loss_fwd_bwd(shard, b[rank], targets, old, ref, adv, w, want_logp=True)
             torch.cuda.synchronize()
-            dfx = (dx.float() - ref_sh).abs()
             allx = [torch.empty_like(mx) for _ in range(world)]
             dist.all_gather(allx, mx)
             ok_fused.append(bool(torch.allclose(lpx, lp_f, atol=2e-6, rtol=2e-6))
                             and bool(torch.allclose(entx, ent_f, atol=2e-5, rtol=2e-5))
-                            and bool((dfx <= ref_sh.abs() * 2 ** -7 + 1e-7).float().mean() > 0.9999)
+                            and grad_ok(dx)
                             and all(torch.equal(m, allx[0]) for m in allx)
                             and bool(torch.allclose(mx[:6], met_f[:6], atol=2e-6, rtol=2e-5)))
         # many rows per CTA (mailbox ring wraps many times), masked rows, fp32

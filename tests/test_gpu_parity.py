@@ -3,6 +3,8 @@
 inputs. Bit-exact for integer/index work (cu_seqlens, seq ids,
 masks, group ids/sizes, replayed expert indices, mismatch counts); stated
 tolerances (tests/_cmp.py) for floating point."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -246,7 +248,7 @@ LOSS_CASES = [
 @pytest.mark.parametrize("case", LOSS_CASES, ids=[c[0] for c in LOSS_CASES])
 def test_pg_loss_fwd_bwd(tm, orc, case):
     _, dtype, V, lens, pkw, kw = case
-    prob = orc.synth_problem(abs(hash(case[0])) % 1000, lens, V, dtype, prompt_max=8)
+    prob = orc.synth_problem(zlib.crc32(case[0].encode()) % 1000, lens, V, dtype, prompt_max=8)  # stable per case
     check_loss_case(tm, orc, prob, pkw, **kw)
 
 
@@ -611,10 +613,11 @@ def test_full_vocab_large_batch_properties(tm, orc):
     assert abs(met[3].item() - wh) <= 1e-5 * abs(wh) + 1e-6
 
 
-@pytest.mark.parametrize("C", [1, 2, 3, 4])
+@pytest.mark.parametrize("C", [2, 3, 4])
 def test_cluster_size_parity(C):
-    """Every cluster size the fused kernel can pick (SFTM_LOSS_C forces one)
-    meets the same parity bar, including the deep run-ahead cases."""
+    """Every multi-CTA cluster size the fused kernel can pick (SFTM_LOSS_C forces
+    one; C = 1 is the default and runs in the main session) meets the same
+    parity bar, including the deep run-ahead cases."""
     import os
     import subprocess
     import sys
@@ -624,36 +627,5 @@ def test_cluster_size_parity(C):
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
                           "test_pg_loss_fwd_bwd or test_pg_loss_deterministic or deep_runahead or step_host or all_rows",
                           "--timeout", "120"],
-                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
-
-
-def test_fwd_ring_baseline_parity():
-    """The older 16-warp ring kernel, kept as the A/B baseline of the forward
-    modes (SFTM_FWD_RING=1), still meets the parity bar."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, SFTM_FWD_RING="1")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
-                          "(test_logprob_fwd and not odd_stride) or vocab_parallel_matches_fused",
-                          "--timeout", "120"],
-                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
-
-
-def test_v3_schedule_parity():
-    """The per-warp software-pipelined schedule (tm_loss3.cu, SFTM_LOSS_VARIANT=3)
-    must meet the same parity bar as the default schedule."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, SFTM_LOSS_VARIANT="3")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
-                          "test_pg_loss_fwd_bwd or test_pg_loss_deterministic or step_host"],
                          cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]

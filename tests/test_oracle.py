@@ -251,3 +251,22 @@ def test_kl_estimators_known_answer(orc, kl_mode):
     assert np.isclose(om[2], (w64 * kl).sum(), rtol=1e-10, atol=1e-14)
     assert np.isclose(om[0], beta * (w64 * kl).sum(), rtol=1e-10, atol=1e-14)
     assert np.allclose(og, w64 * beta * dkl, rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("pkw", [{}, {"beta": 0.05}, {"dual_c": 3.0, "ent_coef": 0.01}, {"beta": 0.1, "kl_mode": 2}])
+def test_metrics_from_rows_matches_oracle(orc, pkw):
+    """tests/_cmp.metrics_from_rows (used by the full-size GPU tests to check the
+    kernel's reduction from its own per-row outputs) restates the oracle's
+    per-row terms exactly."""
+    from tests._cmp import metrics_from_rows
+
+    prob = orc.synth_problem(91, [40, 25, 33], 3000, "f32", prompt_max=10)
+    rng = np.random.default_rng(5)
+    T = prob["T"]
+    a = rng.normal(size=T).astype(np.float32)
+    w = np.where(rng.random(T) < 0.8, 1.0 / T, 0.0).astype(np.float32)
+    p = orc.params(**{k: v for k, v in pkw.items()})
+    om, _, olp, oent, _ = orc.pg_loss_fwd_bwd(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, p)
+    got = metrics_from_rows(olp, oent, prob["old"], prob["ref"], a, w, p.eps_lo, p.eps_hi, p.dual_c, p.beta,
+                            p.ent_coef, p.kl_mode)
+    assert np.allclose(got, om, rtol=1e-12, atol=1e-15)
