@@ -68,6 +68,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Wait for a phase that is usually far off, without the suspend-and-probe loop
+// of mbar_wait: a warp that is ahead of its producer by design (backward
+// warps waiting for a row's scalars, control warps for the partials) would
+// otherwise wake on every mbarrier event of the CTA and re-issue its probe,
+// taking issue slots from the warps on the critical path. ns = 0 keeps the
+// hardware-suspended form.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns) {
+  if (ns == 0) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+
 // Wait with cluster-scope acquire: pairs with remote release-arrives from peer
 // CTAs of the cluster (DSMEM mailbox exchange).
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {

@@ -432,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tph0 = tph;
       bool nobase = false;  // ES: this warp's share of chunk 0 held nothing finite
       (void)tph0;
+
       // One chunk: smem -> registers (slot released at once) -> TMEM stash ->
       // online softmax. `first` sets the exponent base from this thread's max of
       // chunk 0; `partial` masks elements past the slice end. Both are constants
@@ -555,12 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto chunk_es = [&](int k, bool first, bool partial) {
         DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
         const uint32_t sa = ring_t + slot * kCB;
-        const uint4 v0 = lds128(sa);
-        const uint4 v1 = lds128(sa + kCB / 2);
         const int rem = span - k * CE;             // valid elements end here (chunk coordinates)
         const int lo = (UA && k == 0) ? mis : 0;   // ... and start here
         // the warp's maximum of this chunk's valid elements (x * c)
-        auto chunk_max = [&]() {
+        auto chunk_max = [&](uint4 v0, uint4 v1) {
           float x[NE];
           unpack(logits, v0, v1, x);
           float xm = -INFINITY;
@@ -574,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           return xm * c;
         };
         if (first) {
-          m2 = chunk_max();
+          m2 = chunk_max(lds128(sa), lds128(sa + kCB / 2));
           if (!(m2 > -INFINITY)) {  // nothing finite: provisional base, repaired at row end
             m2 = 0.f;
             nobase = true;
@@ -584,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // row-store words (invalid positions 0) and the chunk's partial sums
         uint32_t q[8];
         float2 cs[2], cw[2];
-        auto expo = [&]() {
+        auto expo = [&](uint4 v0, uint4 v1) {
           float x[NE];
           unpack(logits, v0, v1, x);
           cs[0] = cs[1] = cw[0] = cw[1] = make_float2(0.f, 0.f);
@@ -630,13 +629,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         };
-        expo();
+        expo(lds128(sa), lds128(sa + kCB / 2));
         {
           const float2 c01 = __fadd2_rn(cs[0], cs[1]);
           if (__any_sync(0xffffffffu, !(c01.x + c01.y <= kEsMax))) {
             // rare: this chunk rises far above the base. New base = the warp's
-            // maximum of this chunk; rescale the running sums, redo the chunk.
-            const float nb = fmaxf(m2, chunk_max());
+            // maximum of this chunk; rescale the running sums, redo the chunk
+            // (re-read from the ring slot, which is still held).
+            const uint4 r0 = lds128(sa), r1 = lds128(sa + kCB / 2);
+            const float nb = fmaxf(m2, chunk_max(r0, r1));
             const float d = m2 - nb, f = ex2(d);
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               s2[i] = make_float2(s2[i].x * f, s2[i].y * f);
             }
             m2 = nb;
-            expo();
+            expo(r0, r1);
           }
         }
         s2[0] = __fadd2_rn(s2[0], cs[0]);
@@ -662,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sts128(sa2, q0);
           sts128(sa2 + kCB / 2, q1);
         }
-        // the row-store words were computed from v0/v1: both LDS have returned
+        // the row-store words were computed from the slot's LDS: they have returned
         mbar_arrive(empty0 + 8u * slot);
         if (++slot == kSlots) {
           slot = 0;
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) cbase[tph & (ES ? 1u : 0u)][ES ? ts : 0][fw] = m2;
         if (in_tmem) {
-          tmem_wait_st(q0, q1);
+          tmem_wait_st();
           tc_fence_before();
         }
         mbar_arrive(tfull0 + 8u * ts);  // release: orders the smem stores (and cbase) too
@@ -901,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t m = nrow - kXpCredit;
             mbar_wait(smem_u32(&rcv_done[m % kCredD]), (m / kCredD) & 1u);
           }
-          DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u));
+          DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u, a.sleep_ctl_ns));
           Stats v = stats_empty();
           if (lane < kFW) {
             const float4 r = red[rs][lane];
@@ -1029,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // of the row (in-place dlogits stays safe)
       float zy = __int_as_float(0x7fc00000);
       if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
-      DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), rpar));
+      DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&red_bar[rs]), rpar, a.sleep_ctl_ns));
       Stats v = stats_empty();
       if (lane < kFW) {
         const float4 r = red[rs][lane];
@@ -1151,7 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nck_r = UA ? (span + CE - 1) / CE : nck;
       const uint32_t rs = nrow % kRD;
       const uint32_t rpar = (nrow / kRD) & 1u;
-      DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
+      DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&scal_bar[rs]), rpar, a.sleep_bwd_ns));
       const RowScal rsc = scal[rs];
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
@@ -1533,6 +1534,11 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   }
   RowArgs ad = a;
   ad.dbg = debug_counters();
+  static const unsigned sleeps[2] = {
+      [] { const char* v = getenv("SFTM_SLEEP_BWD"); return v ? static_cast<unsigned>(atoi(v)) : 0u; }(),
+      [] { const char* v = getenv("SFTM_SLEEP_CTL"); return v ? static_cast<unsigned>(atoi(v)) : 0u; }()};
+  ad.sleep_bwd_ns = sleeps[0];
+  ad.sleep_ctl_ns = sleeps[1];
   if (ncl > a.max_partial_blocks) ncl = a.max_partial_blocks;
   if (ncl < 1) ncl = 1;
   cudaLaunchConfig_t cfg = {};
@@ -1561,15 +1567,18 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   return e;
 }
 
-// The e-store schedule takes every row whose gradient has no entropy term
+// The e-store schedule can take every row whose gradient has no entropy term
 // (entropy_coef == 0, the DAPO default): the backward then needs p*c0 only.
-// SFTM_ES=0 selects the raw-logit row store for A/B runs.
+// Measured on B200: half the MUFU work and ~180 MHz more SM
+// clock under the power cap, but the forward warps become the critical role
+// and the throughput is 0.5% below the raw-logit store, so it is opt-in
+// (SFTM_ES=1) until the forward/backward warp split is rebalanced.
 inline bool use_es(const RowArgs& a) {
-  static const bool off = [] {
+  static const bool on = [] {
     const char* v = getenv("SFTM_ES");
-    return v && v[0] == '0';
+    return v && v[0] == '1';
   }();
-  return !off && a.ent_coef == 0.f;
+  return on && a.ent_coef == 0.f;
 }
 
 template <typename T, bool ES>

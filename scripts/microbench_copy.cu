@@ -75,7 +75,10 @@ __global__ void __launch_bounds__(288, 1) row_copy(const char* src, char* dst, s
           }
           for (int o = tid * 16; o < chunk; o += 256 * 16) {
             const uint4 v = lds128(rb + slot * chunk + o);
-            __stcs(reinterpret_cast<uint4*>(dst + doff + o), v);
+            if (mode == 3)
+              *reinterpret_cast<uint4*>(dst + doff + o) = v;
+            else
+              __stcs(reinterpret_cast<uint4*>(dst + doff + o), v);
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&empty[slot]));
@@ -107,7 +110,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float ms;
-  for (int bpsm : {4, 8}) {
+  for (int bpsm : {1, 4, 8}) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
       ldg_copy<<<sms * bpsm, 256>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), bytes / 16);
@@ -120,6 +123,9 @@ int main(int argc, char** argv) {
   struct Cfg { int chunk, ns, mode, lag; const char* what; };
   // row_bytes = 151936 B = 12.37 x 12 KB; use chunks dividing it loosely (tail dropped)
   Cfg cfgs[] = {{12288, 17, 0, 0, "TMA ring -> STG same chunk"},
+                {12288, 17, 3, 0, "TMA ring -> STG (no .cs)"},
+                {12288, 8, 0, 0, "TMA ring -> STG 8 slots"},
+                {12288, 8, 1, 0, "TMA ring -> bulk store 8sl"},
                 {8192, 26, 0, 0, "TMA ring -> STG same chunk"},
                 {12288, 17, 1, 0, "TMA ring -> TMA bulk store"},
                 {8192, 26, 1, 0, "TMA ring -> TMA bulk store"},
