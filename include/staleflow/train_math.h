@@ -255,6 +255,15 @@ int sf_tm_r3_gate_bwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64
                       int64_t E, int64_t k, const void* rec_idx, int32_t idx_dtype, int32_t renorm,
                       const float* w, const float* dw, void* dlogits, void* stream);
 
+/* R3 transport ("GPU-resident"): the
+ * rollout's routed_experts bus field is token-major, rec_token_major[T, L, k]
+ * (the concatenated per-sample payloads, copied to the device once); this
+ * writes the gate's layer-major operand rec_layer_major[L, T, k] on the
+ * device, bit-exactly, so the record never makes a host transpose pass.
+ * Out of place. idx_dtype SF_TM_IDX_U8 / _I32. */
+int sf_tm_r3_record_layer_major(sf_tm_t h, const void* rec_token_major, int32_t idx_dtype, int64_t T, int64_t L,
+                                int64_t k, void* rec_layer_major, void* stream);
+
 /* ---- a7: vocab-parallel (logits sharded over P ranks by vocab) ----------
  * Pass 1 (local): per-row partial stats of this rank's shard
  * [vocab_start, vocab_start + Vp): out_stats[T*4] = {max z, sum e^(z-max),
@@ -317,6 +326,8 @@ int sf_tm_vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int
  * Returns ConfigError for bytes == 0 or out == NULL, Internal on CUDA errors. */
 int sf_tm_host_alloc(size_t bytes, void** out);
 int sf_tm_host_free(void* p);
+/* Asynchronous host -> device copy on `stream` (a DMA when src is pinned). */
+int sf_tm_h2d(sf_tm_t h, void* dst, const void* src, size_t bytes, void* stream);
 
 /* ---- synthetic inputs (bench / tests) ------------------------------------
  * Counter-based, seeded with the reference's SplitMix64 (rng.hpp:17-39)

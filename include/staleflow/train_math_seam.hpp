@@ -32,8 +32,11 @@
 
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "staleflow/train_math.h"
@@ -420,6 +423,243 @@ class AdvantageStageSeam {
     }
     payloads.assign(static_cast<size_t>(B), BytesT(sizeof(float)));
     for (int64_t i = 0; i < B; ++i) std::memcpy(payloads[i].data(), ad + i, sizeof(float));
+    return SF_TM_OK;
+  }
+
+ private:
+  sf_tm_t h_ = nullptr;
+  int rc_ = SF_TM_OK;
+  std::string err_;
+  PinnedStage pin_;
+};
+
+
+// ---------------------------------------------------------------------------
+// Group-completion batching. The bus hands samples
+// out FIFO by readiness (proj/src/transfer_queue.cpp:162-175) and sample ids
+// are sequential per permit (proj/src/staleness.cpp:102-106), so a fetched
+// micro-batch can hold any mix of partial groups. GRPO is only defined over a
+// whole group: the Advantages stage (and a trainer that computes GRPO itself)
+// feeds every fetched micro-batch in here and takes back micro-batches made
+// of complete groups only, in the order the groups completed. Group of a
+// sample: its int32 "group" field, else (sample_id - 1) / group_size.
+template <class MicroBatchT>
+class GroupAssembler {
+ public:
+  explicit GroupAssembler(int group_size) : gs_(group_size) {}
+
+  // Buffer every sample of `b` (payloads required). SF_TM_OK, or
+  // SF_TM_CONFIG_ERROR (no payloads, a field set that differs from earlier
+  // batches, a group that receives more than group_size samples).
+  int feed(const MicroBatchT& b, std::string* err) {
+    if (gs_ <= 0) return fail(err, "group_size must be > 0");
+    if (b.payloads.size() != b.sample_ids.size()) return fail(err, "payloads missing (fetch with with_payload=true)");
+    if (fields_.empty()) {
+      fields_ = b.field_set;
+      jg_ = detail::find_field(fields_, "group");
+    } else if (b.field_set != fields_) {
+      return fail(err, "field set changed between micro-batches");
+    }
+    for (size_t i = 0; i < b.sample_ids.size(); ++i) {
+      int64_t g;
+      if (jg_ >= 0) {
+        int32_t v = 0;
+        if (b.payloads[i][jg_].size() != sizeof(v)) return fail(err, "group payload is not int32");
+        std::memcpy(&v, b.payloads[i][jg_].data(), sizeof(v));
+        g = v;
+      } else {
+        g = static_cast<int64_t>((b.sample_ids[i] - 1) / static_cast<uint64_t>(gs_));
+      }
+      auto& bucket = partial_[g];
+      Sample smp{b.sample_ids[i], i < b.producer_versions.size() ? b.producer_versions[i] : Version{},
+                 i < b.global_steps.size() ? b.global_steps[i] : Step{}, b.payloads[i]};
+      bucket.push_back(std::move(smp));
+      if (static_cast<int>(bucket.size()) > gs_)
+        return fail(err, "group " + std::to_string(g) + " received more than " + std::to_string(gs_) + " samples");
+      if (static_cast<int>(bucket.size()) == gs_) {
+        ready_.push_back(std::move(bucket));
+        partial_.erase(g);
+        ready_samples_ += static_cast<size_t>(gs_);
+      }
+    }
+    return SF_TM_OK;
+  }
+
+  // Move up to max_samples samples of complete groups (whole groups only, in
+  // completion order) into `out`. Returns the number of samples moved (0 when
+  // no group is complete or max_samples < group_size).
+  size_t pop(MicroBatchT& out, size_t max_samples) {
+    out = MicroBatchT{};
+    out.batch_id = ++batches_;
+    out.field_set = fields_;
+    size_t n = 0;
+    while (!ready_.empty() && n + static_cast<size_t>(gs_) <= max_samples) {
+      for (auto& smp : ready_.front()) {
+        out.sample_ids.push_back(smp.id);
+        out.producer_versions.push_back(smp.version);
+        out.global_steps.push_back(smp.step);
+        out.payloads.push_back(std::move(smp.row));
+      }
+      ready_.pop_front();
+      n += static_cast<size_t>(gs_);
+    }
+    ready_samples_ -= n;
+    return n;
+  }
+
+  size_t ready_samples() const { return ready_samples_; }
+  size_t pending_groups() const { return partial_.size(); }
+  size_t pending_samples() const {
+    size_t n = 0;
+    for (const auto& kv : partial_) n += kv.second.size();
+    return n;
+  }
+
+ private:
+  using Version = typename std::decay_t<decltype(std::declval<MicroBatchT>().producer_versions)>::value_type;
+  using Step = typename std::decay_t<decltype(std::declval<MicroBatchT>().global_steps)>::value_type;
+  using SampleId = typename std::decay_t<decltype(std::declval<MicroBatchT>().sample_ids)>::value_type;
+  using Row = typename std::decay_t<decltype(std::declval<MicroBatchT>().payloads)>::value_type;
+  struct Sample {
+    SampleId id;
+    Version version;
+    Step step;
+    Row row;
+  };
+  static int fail(std::string* err, const std::string& m) {
+    if (err) *err = m;
+    return SF_TM_CONFIG_ERROR;
+  }
+  int gs_;
+  int jg_ = -1;
+  std::vector<std::string> fields_;
+  std::map<int64_t, std::vector<Sample>> partial_;
+  std::deque<std::vector<Sample>> ready_;
+  size_t ready_samples_ = 0;
+  uint64_t batches_ = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Version-boundary normalisation (the trainer's version boundary
+// fires once consumed_in_version >= G samples, proj/src/sim_runtime.cpp:453-454,
+// 514-557). The DAPO token-mean divides by N = the loss-active tokens of the
+// whole version, which is unknown while its micro-batches stream in. Each
+// micro-batch therefore runs with micro_params() (explicit inv_norm = 1: its
+// dlogits and metrics are unnormalised sums, so the trainer's parameter
+// gradients accumulate unnormalised too); at the boundary close() returns the
+// scale 1/N for the accumulated gradients and the normalised step metrics.
+// By linearity this equals running every micro-batch with inv_norm = 1/N.
+class VersionAccumulator {
+ public:
+  explicit VersionAccumulator(uint64_t global_batch_size) : G_(global_batch_size) {}
+
+  static sf_tm_loss_params micro_params(sf_tm_loss_params p) {
+    p.norm_mode = SF_TM_NORM_EXPLICIT;
+    p.inv_norm = 1.f;
+    return p;
+  }
+  // One micro-batch's metrics (computed with micro_params) and its sample count.
+  void add(const float* h_metrics, uint64_t samples) {
+    for (int i = 0; i < SF_TM_NUM_METRICS; ++i) sum_[i] += static_cast<double>(h_metrics[i]);
+    consumed_ += samples;
+    ++micro_batches_;
+  }
+  bool at_boundary() const { return consumed_ >= G_; }
+  uint64_t consumed() const { return consumed_; }
+
+  struct Closed {
+    uint64_t samples = 0, micro_batches = 0;
+    double active_tokens = 0.0;
+    double grad_scale = 0.0;  // multiply the version's accumulated gradients by this (1/N)
+    double metrics[SF_TM_NUM_METRICS] = {};  // token-means over the version; [SF_TM_M_ACTIVE] = N
+  };
+  Closed close() {
+    Closed c;
+    c.samples = consumed_;
+    c.micro_batches = micro_batches_;
+    c.active_tokens = sum_[SF_TM_M_ACTIVE];
+    c.grad_scale = c.active_tokens > 0 ? 1.0 / c.active_tokens : 0.0;
+    for (int i = 0; i < SF_TM_NUM_METRICS; ++i)
+      c.metrics[i] = (i == SF_TM_M_ACTIVE) ? sum_[i] : sum_[i] * c.grad_scale;
+    for (double& v : sum_) v = 0.0;
+    consumed_ = 0;
+    micro_batches_ = 0;
+    return c;
+  }
+
+ private:
+  uint64_t G_;
+  uint64_t consumed_ = 0, micro_batches_ = 0;
+  double sum_[SF_TM_NUM_METRICS] = {};
+};
+
+// ---------------------------------------------------------------------------
+// R3 routed-experts transport (the paper keeps the record
+// GPU-resident). The samples' routed_experts payloads are
+// token-major, so their bus-order concatenation IS the token-major record
+// [T, layers, k]: it is staged with one memcpy per sample (no per-byte host
+// transpose, unlike pack_routed_experts), copied to the device once, and
+// transposed to the gate's layer-major operand there
+// (sf_tm_r3_record_layer_major). d_tok: caller-owned device scratch of
+// T * layers * k bytes; d_rec: the layer-major u8 [layers, T, k] output.
+class RoutedExpertsSeam {
+ public:
+  explicit RoutedExpertsSeam(int device = 0) { rc_ = sf_tm_create(device, &h_); }
+  ~RoutedExpertsSeam() {
+    if (h_) sf_tm_destroy(h_);
+  }
+  RoutedExpertsSeam(const RoutedExpertsSeam&) = delete;
+  RoutedExpertsSeam& operator=(const RoutedExpertsSeam&) = delete;
+  int status() const { return rc_; }
+  sf_tm_t handle() const { return h_; }
+  const std::string& error() const { return err_; }
+
+  // Token count of the batch's record (sum of response lengths), or -1 with error().
+  template <class MicroBatchT>
+  int64_t tokens(const MicroBatchT& b, int layers, int k) {
+    const int jr = detail::find_field(b.field_set, "response");
+    const int je = detail::find_field(b.field_set, "routed_experts");
+    if (jr < 0 || je < 0 || layers <= 0 || k <= 0 || b.payloads.size() != b.sample_ids.size()) {
+      err_ = "routed_experts needs the response and routed_experts fields (with payloads) and layers, k > 0";
+      return -1;
+    }
+    int64_t T = 0;
+    for (size_t i = 0; i < b.payloads.size(); ++i) {
+      const size_t L = b.payloads[i][jr].size() / sizeof(int32_t);
+      if (b.payloads[i][je].size() != L * static_cast<size_t>(layers) * k) {
+        err_ = "sample " + std::to_string(b.sample_ids[i]) + ": routed_experts is not L*layers*k bytes";
+        return -1;
+      }
+      T += static_cast<int64_t>(L);
+    }
+    return T;
+  }
+
+  // Stage + copy + device transpose; asynchronous on `stream` (the pinned
+  // staging is reused by the next call only after this one's copy finished).
+  template <class MicroBatchT>
+  int upload(const MicroBatchT& b, int layers, int k, void* d_tok, void* d_rec, int64_t* T_out, void* stream) {
+    if (rc_ != SF_TM_OK) return rc_;
+    const int64_t T = tokens(b, layers, k);
+    if (T < 0) return SF_TM_CONFIG_ERROR;
+    if (T_out) *T_out = T;
+    const size_t bytes = static_cast<size_t>(T) * layers * k;
+    if (bytes == 0) return SF_TM_OK;
+    int rc = sf_tm_sync(h_, stream);  // the previous upload's copy has read the staging
+    if (rc) return rc;
+    auto* st = static_cast<uint8_t*>(pin_.get(0, bytes, &rc));
+    if (rc) return rc;
+    const int je = detail::find_field(b.field_set, "routed_experts");
+    size_t off = 0;
+    for (const auto& row : b.payloads) {
+      std::memcpy(st + off, row[je].data(), row[je].size());
+      off += row[je].size();
+    }
+    if ((rc = sf_tm_h2d(h_, d_tok, st, bytes, stream)) ||
+        (rc = sf_tm_r3_record_layer_major(h_, d_tok, SF_TM_IDX_U8, T, layers, k, d_rec, stream))) {
+      err_ = sf_tm_last_error(h_);
+      return rc;
+    }
     return SF_TM_OK;
   }
 

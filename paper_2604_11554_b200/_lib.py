@@ -88,6 +88,7 @@ _SIGS = {
     ),
     "sf_tm_r3_gate_fwd": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "sf_tm_r3_gate_bwd": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "sf_tm_r3_record_layer_major": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _vp, _vp]),
     "sf_tm_vp_partial_stats": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _f32, _vp, _vp]),
     "sf_tm_vp_loss_fwd_bwd": (
         ctypes.c_int,
@@ -110,6 +111,7 @@ _SIGS = {
     "sf_tm_synth_logits": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _u64, _f32, _vp, _f32, _f32, _f32, _vp]),
     "sf_tm_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "sf_tm_host_free": (ctypes.c_int, [_vp]),
+    "sf_tm_h2d": (ctypes.c_int, [_H, _vp, _vp, ctypes.c_size_t, _vp]),
     "sf_tm_debug_force_generic": (ctypes.c_int, [ctypes.c_int]),
     "sf_tm_debug_wait_counters": (ctypes.c_int, [_vp]),
 }

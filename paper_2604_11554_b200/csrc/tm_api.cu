@@ -734,6 +734,25 @@ int sf_tm_r3_gate_bwd(sf_tm_t h, const void* router_logits, int32_t dtype, int64
   return check_cuda(h, e, "sf_tm_r3_gate_bwd");
 }
 
+int sf_tm_r3_record_layer_major(sf_tm_t h, const void* rec_token_major, int32_t idx_dtype, int64_t T, int64_t L,
+                                int64_t k, void* rec_layer_major, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (idx_dtype != SF_TM_IDX_I32 && idx_dtype != SF_TM_IDX_U8)
+    return fail(h, SF_TM_CONFIG_ERROR, "idx_dtype must be SF_TM_IDX_*");
+  if (T < 0 || L < 0) return fail(h, SF_TM_CONFIG_ERROR, "T and L must be >= 0");
+  if (k < 1 || k > 32) return fail(h, SF_TM_CONFIG_ERROR, "k must be in [1, 32]");
+  if (T > 65535LL * 32 * 1024 || L > 65535LL * 32) return fail(h, SF_TM_CONFIG_ERROR, "T or L too large");
+  if (T * L == 0) return SF_TM_OK;
+  if (!rec_token_major || !rec_layer_major) return fail(h, SF_TM_CONFIG_ERROR, "record pointers are required");
+  if (rec_token_major == rec_layer_major) return fail(h, SF_TM_CONFIG_ERROR, "the transpose is out of place");
+  int n = 0;
+  const int e = sftm::launch_rec_layer_major(rec_token_major, idx_dtype, T, L, k, rec_layer_major,
+                                             static_cast<cudaStream_t>(stream), &n);
+  h->launches += n;
+  return check_cuda(h, e, "sf_tm_r3_record_layer_major");
+}
+
 int sf_tm_vp_partial_stats(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T,
                            int64_t Vp, int64_t ld, int64_t vocab_start, const int32_t* targets,
                            float inv_temperature, float* out_stats, void* stream) {
@@ -960,6 +979,15 @@ int sf_tm_host_alloc(size_t bytes, void** out) {
 int sf_tm_host_free(void* p) {
   if (!p) return SF_TM_OK;
   return cudaFreeHost(p) == cudaSuccess ? SF_TM_OK : SF_TM_INTERNAL;
+}
+
+int sf_tm_h2d(sf_tm_t h, void* dst, const void* src, size_t bytes, void* stream) {
+  if (!h) return SF_TM_CONFIG_ERROR;
+  if (int rc = use_device(h)) return rc;
+  if (bytes == 0) return SF_TM_OK;
+  if (!dst || !src) return fail(h, SF_TM_CONFIG_ERROR, "sf_tm_h2d: NULL pointer");
+  return check_cuda(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
+                    "sf_tm_h2d");
 }
 
 int sf_tm_debug_force_generic(int on) {

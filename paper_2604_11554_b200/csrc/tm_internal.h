@@ -145,6 +145,10 @@ int launch_r3_bwd(const void* logits, int dtype, int64_t L, int64_t T, int64_t E
                   const void* rec_idx, int idx_dtype, int renorm, const float* w, const float* dw,
                   void* dlogits, cudaStream_t s, int* launches);
 
+// routed_experts record, token-major [T, L, k] -> layer-major [L, T, k] (bit-exact)
+int launch_rec_layer_major(const void* rec_tok, int idx_dtype, int64_t T, int64_t L, int64_t k, void* rec_layer,
+                           cudaStream_t s, int* launches);
+
 int launch_synth_logits(void* logits, int dtype, int64_t T, int64_t V, int64_t ld, uint64_t seed,
                         float sigma, const int32_t* peak_id, float peak_lo, float peak_hi,
                         float outlier_frac, cudaStream_t s, int* launches);

@@ -170,6 +170,63 @@ int launch_grpo_advantage(const float* rewards, const int32_t* group_ids, int64_
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ a5 transport
+// The rollout records routed experts per token ("routed_experts" bus field:
+// token-major [T, L, k]); the gate consumes them
+// layer-major [L, T, k]. After ONE host->device copy of the concatenated
+// payloads, a 32 x 32 record tile goes through shared memory per CTA: reads
+// are contiguous along layers, writes contiguous along tokens. Records move
+// as whole 4- or 8-byte words when their size allows (k u8 indices, or k
+// int32), else bytewise. Bit-exact by construction.
+template <typename W>
+__global__ void __launch_bounds__(256)
+    rec_transpose_kernel(const W* __restrict__ src, W* __restrict__ dst, int64_t Tn, int64_t L, int wpr) {
+  extern __shared__ __align__(16) unsigned char tile_raw[];
+  W* tile = reinterpret_cast<W*>(tile_raw);  // [32 t][32 l][wpr] (+1 word pad per t row)
+  const int pitch = 32 * wpr + 1;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32, l0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int nw = 32 * wpr;  // words per tile row
+  for (int i = threadIdx.x; i < 32 * nw; i += blockDim.x) {
+    const int tt = i / nw, r = i % nw;  // token row of the tile, word within its 32 layers
+    const int64_t t = t0 + tt, l = l0 + r / wpr;
+    if (t < Tn && l < L) tile[tt * pitch + r] = src[(t * L + l) * wpr + r % wpr];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * nw; i += blockDim.x) {
+    const int ll = i / nw, r = i % nw;  // layer row of the tile, word within its 32 tokens
+    const int64_t l = l0 + ll, t = t0 + r / wpr;
+    if (t < Tn && l < L) dst[(l * Tn + t) * wpr + r % wpr] = tile[(r / wpr) * pitch + ll * wpr + r % wpr];
+  }
+}
+
+int launch_rec_layer_major(const void* rec_tok, int idx_dtype, int64_t T, int64_t L, int64_t k, void* rec_layer,
+                           cudaStream_t s, int* launches) {
+  const int64_t rb = k * (idx_dtype == 1 ? 1 : 4);  // bytes per (token, layer) record
+  const uintptr_t al = reinterpret_cast<uintptr_t>(rec_tok) | reinterpret_cast<uintptr_t>(rec_layer);
+  const dim3 grid(static_cast<unsigned>((T + 31) / 32), static_cast<unsigned>((L + 31) / 32));
+  auto go = [&](auto w) {
+    using Wt = decltype(w);
+    const int wpr = static_cast<int>(rb / static_cast<int64_t>(sizeof(Wt)));
+    const size_t smem = sizeof(Wt) * 32 * static_cast<size_t>(32 * wpr + 1);  // <= 129 KB (k = 32 int32)
+    static PerDevice opted;  // per instantiation and device: allow > 48 KB dynamic smem
+    if (opted() < 0) {
+      cudaFuncSetAttribute(rec_transpose_kernel<Wt>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+      opted() = 1;
+    }
+    rec_transpose_kernel<Wt><<<grid, 256, smem, s>>>(static_cast<const Wt*>(rec_tok), static_cast<Wt*>(rec_layer),
+                                                     T, L, wpr);
+  };
+  if (rb % 8 == 0 && al % 8 == 0) {
+    go(uint64_t{});
+  } else if (rb % 4 == 0 && al % 4 == 0) {
+    go(uint32_t{});
+  } else {
+    go(uint8_t{});
+  }
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ a4 prologue
 // Pass 1: active-token count per sequence; the last block reduces the totals
 // (sum of counts, number of sequences with >= 1 active token) in seq order.

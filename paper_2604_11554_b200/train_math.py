@@ -258,6 +258,21 @@ def r3_gate_bwd(router_logits, rec_idx, w, dw, renorm: bool = True, out=None):
     return dz
 
 
+def r3_record_layer_major(rec_token_major: torch.Tensor, out: Optional[torch.Tensor] = None):
+    """routed_experts record [T, L, k] (token-major, as on the bus) -> the gate's
+    layer-major [L, T, k], on the device, bit-exact."""
+    d = _dev(rec_token_major)
+    h = handle(d)
+    T, L, k = rec_token_major.shape
+    it = _lib.IDX_U8 if rec_token_major.dtype == torch.uint8 else _lib.IDX_I32
+    src = rec_token_major.contiguous()
+    if out is None:
+        out = torch.empty(L, T, k, dtype=rec_token_major.dtype, device=rec_token_major.device)
+    rc = _lib.lib().sf_tm_r3_record_layer_major(h.ptr, _p(src), it, T, L, k, _p(out), _stream(d))
+    h.check(rc, "sf_tm_r3_record_layer_major")
+    return out
+
+
 # ---------------------------------------------------------------------- a7
 def vp_partial_stats(shard, targets, vocab_start: int, inv_temperature: float = 1.0):
     d = _dev(shard)

@@ -245,3 +245,24 @@ def test_config4_omni_long_sequences(tm, orc):
     assert_grad_close(grad_np(dl[rows]), odl, scale, "bf16", rows_ok=~near)
     del logits, dl
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------------------- a5 transport (f4)
+@pytest.mark.parametrize("T,L,k,dt", [(2048, 48, 8, "u8"), (301, 5, 3, "u8"), (77, 33, 16, "i32"), (1000, 7, 32, "i32"),
+                                      (33, 48, 1, "u8"), (4096, 48, 8, "i32")])
+def test_r3_record_token_to_layer_major_bit_exact(tm, orc, T, L, k, dt):
+    """The routed_experts record as the bus carries it (token-major [T, L, k])
+    transposed on the device to the gate's layer-major [L, T, k]: FNV digest
+    equal to the host transpose, and the gate on it equal to the gate on the
+    host-transposed record."""
+    rng = np.random.default_rng(T + L + k)
+    npdt = np.uint8 if dt == "u8" else np.int32
+    rec_tok = rng.integers(0, 128, size=(T, L, k)).astype(npdt)
+    out = tm.r3_record_layer_major(torch.from_numpy(rec_tok).cuda())
+    host = np.ascontiguousarray(rec_tok.transpose(1, 0, 2))
+    assert orc.digest(out.cpu().numpy()) == orc.digest(host)
+    if k <= 16 and dt == "u8":
+        z = torch.from_numpy((rng.normal(size=(L, T, 128)) * 2).astype(np.float32)).cuda()
+        w1, i1, m1 = tm.r3_gate_fwd(z, out)
+        w2, i2, m2 = tm.r3_gate_fwd(z, torch.from_numpy(host).cuda())
+        assert torch.equal(w1, w2) and torch.equal(i1, i2) and torch.equal(m1, m2)
