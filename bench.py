@@ -14,12 +14,20 @@ micro-batch the fused loss fwd+bwd writing dlogits. The per-micro-batch logits
 output, which never crosses the bus — and are far larger than L2 (126 MB), so
 no L2 flush is needed between steps. Data are synthetic (seeded SplitMix64).
 
+`value` counts loss-active tokens (mask = 1); `value_all_tokens`
+adds the masked prompt rows. `e2e` is the same metric through the C++ trainer
+seam (ActorLossSeam::step via libsf_seam.so) on MicroBatch payloads as the bus
+delivers them, host->device copies included.
+
 Multi-GPU: one process per GPU (torchrun), weak scaling — each rank processes
-its own global batch; the only exchange is one all-reduce of the step metrics.
+its own global batch of sequences; before the step the ranks sum their
+loss-active token counts (one 8-byte all-reduce) so every rank weights by the
+global token-mean, and after it one all-reduce of the step metrics.
 
 `--impl reference`: the reference has no implementation of this path
-(SPEC.md:8); its CPU arm is the repo's fp64 C oracle port (oracle/), run on all
-host cores on a bounded sample of the same workload.
+(SPEC.md:8); its CPU arm is the repo's fp32 port of the oracle (oracle/), run on
+all host threads on 4,096 rows of the same workload per step (>= 10 s timed),
+with the CPU model and a one-thread rate recorded.
 """
 from __future__ import annotations
 
@@ -131,8 +139,50 @@ def make_step_inputs(rng: np.random.Generator, n_seq: int, L: int, V: int, G: in
     return T, lens, plens, rewards, gids
 
 
+def cpu_model() -> str:
+    """The host CPU model (the CPU baseline depends on it; boxes differ)."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _time_cpu(run, target_s: float):
+    """Repeat run() until ~target_s of CPU time has been measured; (passes, seconds)."""
+    run()  # warm (page-in, thread pool)
+    reps, dt = 0, 0.0
+    while dt < target_s or reps == 0:
+        t0 = time.perf_counter()
+        run()
+        dt += time.perf_counter() - t0
+        reps += 1
+    return reps, dt
+
+
+def cpu_rate_one_thread(orc, smp, target_s: float = 3.0):
+    """Tokens/s of the same CPU port on ONE thread (a slice of the sample)."""
+    cores = os.cpu_count() or 1
+    rows = max(1, min(len(smp[0]), 16))
+    sub = tuple(a[:rows] for a in smp)
+    orc.set_threads(1)
+    try:
+        reps, dt = _time_cpu(lambda: orc.pg_loss_fwd_bwd_fast(*sub, orc.params()), target_s)
+    finally:
+        orc.set_threads(cores)
+    return rows * reps / dt
+
+
 def run_reference(args, rank: int):
-    """CPU arm: the fp64 oracle port on all host cores, bounded sample per step."""
+    """CPU arm: the oracle's fp32 CPU port (the reference has no implementation of
+    this path) on all host threads, on rows of the same workload
+    (V = 151,936 bf16, every row loss-active). Each step is 4,096 rows -- the
+    cpu_baseline leg's sample -- repeated so the timed steps hold >= 10 s of CPU
+    work in total; the run stays within a few minutes."""
     if rank != 0:
         return
     from oracle import oracle as orc
@@ -140,24 +190,25 @@ def run_reference(args, rank: int):
     orc.lib()
     cores = os.cpu_count() or 1
     orc.set_threads(cores)
-    rows = max(8 * cores, 128)
+    rows = 4096
     prob = orc.synth_problem(7, [rows], args.vocab, "bf16", prompt_max=0)
     a = np.random.default_rng(0).normal(size=rows).astype(np.float32)
     w = np.full(rows, 1.0 / rows, np.float32)
+    smp = (prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w)
     p = orc.params()
+    one = lambda: orc.pg_loss_fwd_bwd_fast(*smp, p)
+    one()  # warm
+    t0 = time.perf_counter()
+    one()
+    t_pass = time.perf_counter() - t0
+    passes = max(1, int(np.ceil(10.0 / max(args.steps, 1) / t_pass)))  # >= 10 s over the timed steps
+    budget = 240.0 / max(1, args.steps + args.warmup)  # the whole run within a few minutes
+    passes = max(1, min(passes, int(budget / t_pass)))
 
     def step():
-        orc.pg_loss_fwd_bwd_fast(prob["logits"], prob["targets"], prob["old"], prob["ref"], a, w, p)
+        for _ in range(passes):
+            one()
 
-    t0 = time.perf_counter()
-    step()
-    one = time.perf_counter() - t0
-    # scale the sample so the whole --steps/--warmup run stays within a few minutes
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    if one > budget and rows > 8:
-        rows = max(8, int(rows * budget / one))
-        prob = orc.synth_problem(7, [rows], args.vocab, "bf16", prompt_max=0)
-        a, w = a[:rows], np.full(rows, 1.0 / rows, np.float32)
     for _ in range(args.warmup):
         step()
     ts = []
@@ -166,15 +217,18 @@ def run_reference(args, rank: int):
         step()
         ts.append(time.perf_counter() - t0)
     sec = float(np.mean(ts))
-    tok_s = rows / sec
-    sample = f"{rows} rows x V={args.vocab} bf16 per step (fused loss fwd+bwd, fp32 vectorised CPU port, OpenMP)"
+    tok_s = rows * passes / sec
+    one_thread = cpu_rate_one_thread(orc, smp)
+    sample = (f"{rows} loss-active rows x V={args.vocab} bf16, x {passes} passes per step "
+              f"({sum(ts):.1f} s timed), fused loss fwd+bwd, fp32 vectorised CPU port (oracle/sf_cpu_fast.c), OpenMP")
     out = {
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded SplitMix64)",
-        "config": {"workload": "Qwen3-4B shape (BASELINE configs[1]) row sample", "vocab": args.vocab,
-                   "rows_per_step": rows, "logits": "bf16"},
-        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "config": {"workload": "Qwen3-4B shape (BASELINE configs[1]) row sample, every row loss-active",
+                   "vocab": args.vocab, "rows_per_step": rows * passes, "logits": "bf16"},
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model(), "value_1thread": one_thread},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
         "note": "the reference has no implementation of this path (SPEC.md:8); the timed CPU arm is the fp32 "
@@ -184,7 +238,8 @@ def run_reference(args, rank: int):
 
 
 def cpu_baseline_leg(tm, logits, targets, old, ref, adv_tok, w_tok, vocab, target_s):
-    """Time the oracle on rows copied from the device workload (same data)."""
+    """Time the CPU port on loss-active rows copied from the device workload
+    (same data): all host threads, and one thread."""
     import torch
     from oracle import oracle as orc
 
@@ -199,28 +254,14 @@ def cpu_baseline_leg(tm, logits, targets, old, ref, adv_tok, w_tok, vocab, targe
         return (sub, targets[idx].cpu().numpy(), old[idx].cpu().numpy(), ref[idx].cpu().numpy(),
                 adv_tok[idx].cpu().numpy(), w_tok[idx].cpu().numpy())
 
-    n = max(cores, 8)
+    n = 4096  # <= 2.5 GB of host logits + dlogits
     s = sample(n)
-    run = lambda smp: orc.pg_loss_fwd_bwd_fast(*smp, orc.params())  # fp32 vectorised variant
-    run(s)  # warm (page-in, thread pool)
-    t0 = time.perf_counter()
-    run(s)
-    dt = time.perf_counter() - t0
-    n2 = int(min(max(n, n * target_s / max(dt, 1e-3)), 4096))  # <= 2.5 GB of host logits
-    if n2 > n:
-        s = sample(n2)
-        n = n2
-    # repeat the bounded sample until ~target_s of CPU work has been timed
-    reps, dt = 0, 0.0
-    while dt < target_s or reps == 0:
-        t0 = time.perf_counter()
-        run(s)
-        dt += time.perf_counter() - t0
-        reps += 1
-    n_done = n * reps
-    return {"value": n_done / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
+    reps, dt = _time_cpu(lambda: orc.pg_loss_fwd_bwd_fast(*s, orc.params()), target_s)
+    one_thread = cpu_rate_one_thread(orc, s)
+    return {"value": n * reps / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
             "sample": f"{n} loss-active rows of the timed workload (V={vocab} bf16) x {reps} passes, fused fwd+bwd "
-                      f"with the fp32 vectorised CPU port (oracle/sf_cpu_fast.c), {dt:.1f} s on {cores} threads"}
+                      f"with the fp32 vectorised CPU port (oracle/sf_cpu_fast.c), {dt:.1f} s on {cores} threads",
+            "cpu_model": cpu_model(), "value_1thread": one_thread}
 
 
 def main():
@@ -235,7 +276,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2604_11554_b200 import _lib, train_math as tm
+    from paper_2604_11554_b200 import _lib, data_parallel as dp, train_math as tm
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -283,7 +324,10 @@ def main():
     d_rewards = torch.from_numpy(rewards).to(dev)
     d_gids = torch.from_numpy(gids).to(dev)
     n_active = int((lens - np.minimum(plens, lens)).sum())
-    inv_norm = 1.0 / n_active  # DAPO token-mean over the whole step (H5: exact)
+    # DAPO token-mean over the whole GLOBAL step (H5: exact): every rank weights
+    # its tokens by 1 / (loss-active tokens summed over the ranks)
+    n_active_global = dp.global_active_tokens(n_active, device=dev)
+    inv_norm = 1.0 / n_active_global
     params = _lib.default_loss_params(norm_mode=_lib.NORM_EXPLICIT, inv_norm=inv_norm)
     if args.generic:
         tm.set_force_generic(True)
@@ -338,7 +382,8 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     ms_step = ms_max / args.steps
-    value = world * T_step / (ms_step / 1e3)
+    value = n_active_global / (ms_step / 1e3)  # loss-active tokens of all ranks
+    value_all = world * T_step / (ms_step / 1e3)  # every token, masked prompt rows included
 
     # roofline of the dominant kernel (fused loss fwd+bwd), algorithmic bytes per launch
     es = 2
@@ -369,24 +414,31 @@ def main():
             traffic = None
     kernel_share = sum(kms) / ms if ms > 0 else None
 
-    # ---------------- end-to-end through the host-buffer C-ABI call (e2e)
+    # ---------------- end-to-end through the C++ trainer seam (e2e): per micro-batch
+    # ActorLossSeam::step (include/staleflow/train_math_seam.hpp) on the MicroBatch
+    # as the bus delivers it (payload bytes of the trainer field set, built once
+    # outside the timed region): payload decode, pinned staging, H2D, GRPO over the
+    # micro-batch's complete groups, token weights, fused loss, D2H metrics.
     e2e = None
     if not args.no_e2e:
-        h_t = targets.cpu().pin_memory()
-        h_o = old.cpu().pin_memory()
-        h_r = ref.cpu().pin_memory()
-        h_lens = torch.from_numpy(lens).pin_memory()
-        h_pl = torch.from_numpy(plens).pin_memory()
-        h_rw = torch.from_numpy(rewards).pin_memory()
-        h_g = torch.from_numpy(gids).pin_memory()
+        from paper_2604_11554_b200 import seam
+
+        actor = seam.ActorLossSeam(local)
+        h_t, h_o, h_r = targets.cpu().numpy(), old.cpu().numpy(), ref.cpu().numpy()
+        tok_mask = np.ones(T_step, np.uint8)
+        for b_ in range(n_seq):
+            tok_mask[b_ * L:b_ * L + min(int(plens[b_]), L)] = 0
+        batches = []
+        for m in range(M):
+            sl = slice(m * T_mb, (m + 1) * T_mb)
+            ss = slice(m * S, (m + 1) * S)
+            batches.append(seam.MicroBatch(lens[ss], h_t[sl], h_o[sl], h_r[sl], rewards[ss], False,
+                                           loss_mask=tok_mask[sl], sample_ids=np.arange(m * S, (m + 1) * S) + 1))
         h_met = torch.zeros(M, _lib.NUM_METRICS).pin_memory()
 
         def e2e_step():
             for m in range(M):
-                sl = slice(m * T_mb, (m + 1) * T_mb)
-                ss = slice(m * S, (m + 1) * S)
-                tm.pg_step_host(logits, h_t[sl], h_o[sl], h_r[sl], h_lens[ss], h_rw[ss], h_g[ss],
-                                h_prompt_lens=h_pl[ss], params=params, dlogits=dlogits, h_metrics=h_met[m])
+                actor.step(batches[m], logits, dlogits, params, h_met[m], group_size=G)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -402,17 +454,22 @@ def main():
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_step = float(ems.item()) / args.steps
-        h2d = T_step * (4 + 4 + 4) + n_seq * (4 * 4)
+        h2d = T_step * (4 + 4 + 4 + 1) + n_seq * (4 + 4 + 4)  # targets, logp, ref_logp, loss_mask; lens, reward, group
         d2h = M * _lib.NUM_METRICS * 4
-        e2e = {"value": world * T_step / (e_step / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+        # the seam's metrics equal the device path's (same groups, same weights)
+        e_met = h_met.sum(0)
+        e2e = {"value": n_active_global / (e_step / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_step,
-               "path": "sf_tm_pg_step_host per micro-batch (pinned host bus fields -> H2D -> varlen/GRPO/"
-                       "weights/fused loss -> D2H metrics); logits device-resident (LM-head output)"}
+               "value_all_tokens": world * T_step / (e_step / 1e3),
+               "loss_matches_device_path": bool(abs(float(e_met[0]) - float(metrics.sum(0)[0].item())) <=
+                                                1e-5 * abs(float(e_met[0])) + 1e-7),
+               "path": "C++ ActorLossSeam::step per micro-batch via libsf_seam.so (MicroBatch payload bytes of "
+                       "the trainer field set -> decode -> pinned staging -> H2D -> varlen/GRPO/weights/fused "
+                       "loss -> D2H metrics); logits device-resident (LM-head output)"}
 
-    # step metrics all-reduce (the one real DP exchange); metrics of the last device step
-    step_metrics = metrics.sum(0)
-    if world > 1:
-        dist.all_reduce(step_metrics)
+    # step metrics all-reduce (the one real DP exchange); metrics of the last device step,
+    # weighted by the global token count, so the SUM is the global token-mean
+    step_metrics = dp.reduce_step_metrics(metrics.sum(0))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -431,7 +488,10 @@ def main():
             "config": {"workload": "Qwen3-4B shape, BASELINE configs[1]: 64 prompts x 8 rollouts x 4096 tok per rank",
                        "vocab": V, "global_batch_seqs": world * n_seq, "seq_len": L,
                        "micro_batches": M, "seqs_per_micro_batch": S, "tokens_per_step": world * T_step,
-                       "loss_active_tokens_per_step": world * n_active, "parallelism": f"dp{world} (sequence sharding)",
+                       "loss_active_tokens_per_step": n_active_global,
+                       "value_counts": "loss-active tokens (mask = 1, SURVEY.md §8d); value_all_tokens adds the "
+                                       "masked prompt rows",
+                       "parallelism": f"dp{world} (sequence sharding, global token-mean)",
                        "l2": "no flush: 39.8 GB resident logits per launch >> 126 MB L2",
                        "loss": "DAPO decoupled clip 0.2/0.28, token-mean over step, beta=0",
                        "kernel": "generic two-pass" if args.generic else
@@ -442,6 +502,7 @@ def main():
                          "avg_launch_ms": avg_kms, "kernel_share_of_step": kernel_share,
                          "bytes_model": "4V B per loss-active row (bf16 read + dlogits write), 2V B per masked row "
                                         "(zero-filled dlogits), + 20 B/token scalars"},
+            "value_all_tokens": value_all,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -128,7 +128,10 @@ def run_loss_config(args, cfg, world, rank, dev, dist):
     ref = (logp0 + 0.1 * torch.randn(T, device=dev, generator=g)).float()
     d_lens, d_rw, d_g = (torch.from_numpy(x).to(dev) for x in (lens, rewards, gids))
     d_mask = torch.from_numpy(mask).to(dev)
-    n_act = int(mask.sum())
+    from paper_2604_11554_b200 import data_parallel as dp
+
+    n_act_local = int(mask.sum())
+    n_act = dp.global_active_tokens(n_act_local, device=dev)  # global token-mean over the ranks
     params = _lib.default_loss_params(norm_mode=_lib.NORM_EXPLICIT, inv_norm=1.0 / n_act, kl_beta=beta)
     metrics = torch.zeros(M, _lib.NUM_METRICS, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -155,13 +158,14 @@ def run_loss_config(args, cfg, world, rank, dev, dist):
     ms_step, kms, clocks = _timed(step, args.steps, args.warmup, dev, world, dist, stream)
     launches = h.launch_count() - l0
     pk, src = _peak()
-    act_mb = [int(mask[m * T_mb:(m + 1) * T_mb].sum()) for m in range(M)]
+    act_mb = [int(mask[m * T_mb:(m + 1) * T_mb].sum()) for m in range(M)]  # this rank's rows
     by = float(np.mean([a * 2 * V * es + (T_mb - a) * V * es + 20 * T_mb for a in act_mb]))
     ach = by / (kms / 1e3) / 1e9
     _line(args, world, METRIC_LOSS if cfg == 4 else METRIC_LOSS.replace("(Qwen3-4B vocab)", "(32k vocab, fp32)"),
-          world * T / (ms_step / 1e3), ms_step, "bf16" if es == 2 else "f32",
+          n_act / (ms_step / 1e3), ms_step, "bf16" if es == 2 else "f32",
           {"workload": workload, "config_index": cfg, "vocab": V, "tokens_per_step": world * T,
-           "loss_active_tokens_per_step": world * n_act, "micro_batches": M, "kl_beta": beta,
+           "loss_active_tokens_per_step": n_act, "value_counts": "loss-active tokens",
+           "value_all_tokens": world * T / (ms_step / 1e3), "micro_batches": M, "kl_beta": beta,
            "l2": "inputs >> L2 (no flush)", "parallelism": f"dp{world}"},
           {"bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk, "traffic": None,
            "peak_source": src, "algorithmic_bytes_per_launch": by, "avg_launch_ms": kms,
@@ -278,36 +282,55 @@ def run_r3(args, world, rank, dev, dist):
 
 
 def run_vocab_parallel(args, world, rank, dev, dist):
-    """Config 5: vocab-parallel fused loss over P = world ranks (strong scaling)."""
+    """Config 5 as BASELINE.json states it: the vocab-parallel loss over P = world
+    ranks (strong scaling: every rank holds a 1/P vocab shard of the SAME tokens)
+    for one global step of 256 prompts x 16 rollouts = 4,096 packed sequences of
+    1,024 tokens (4,194,304 tokens; 32 micro-batches of 128 sequences), GRPO over
+    the 256 groups of 16, DAPO token-mean over the step, staleness-tagged samples
+    (producer versions v_t - {0, 1, 2}; the per-micro-batch staleness histogram
+    and batch staleness come from the C++ seam, staleness_histogram =
+    StalenessGate::staleness_of, proj/src/staleness.cpp:169-173)."""
     import torch
 
-    from paper_2604_11554_b200 import _lib, train_math as tm
+    from paper_2604_11554_b200 import _lib, seam, train_math as tm
     from paper_2604_11554_b200.vocab_parallel import gather_stats, open_peer_exchange, shard_bounds
 
     V, P = 151936, world
     b = shard_bounds(V, P)
     vs, Vp = b[rank], b[rank + 1] - b[rank]
-    M, S, Ls = 4, 32, 4096
+    prompts, G, Ls, S = 256, 16, 1024, 128
+    n_seq = prompts * G
+    M = n_seq // S
     T_mb = S * Ls
     T = M * T_mb
     rng = np.random.default_rng(3000)  # same token data on every rank
     shard = torch.empty(T_mb, Vp, dtype=torch.bfloat16, device=dev)
     tm.synth_logits(shard, seed=900 + rank, sigma=2.0)
     targets = torch.from_numpy(rng.integers(0, V, size=T).astype(np.int32)).to(dev)
-    plens = rng.integers(32, 513, size=M * S)
+    plens = rng.integers(32, 257, size=n_seq)
     mask = np.ones(T, np.uint8)
-    for s_ in range(M * S):
+    for s_ in range(n_seq):
         mask[s_ * Ls:s_ * Ls + plens[s_]] = 0
     n_act = int(mask.sum())
-    # staleness tags (a8): producer versions of the samples vs trainer version
+    rewards = (rng.random(n_seq) < 0.5).astype(np.float32)
+    gids = (np.arange(n_seq) // G).astype(np.int32)
+    # staleness tags (a8): producer versions of the samples vs trainer version v_t
     v_t = 10
-    prod_ver = v_t - rng.choice([0, 0, 0, 1, 1, 2], size=M * S)
-    stale_hist = {int(s): int(c) for s, c in zip(*np.unique(v_t - prod_ver, return_counts=True))}
+    prod_ver = (v_t - rng.choice([0, 0, 0, 1, 1, 2], size=n_seq)).astype(np.int64)
+    hist = np.zeros(8, np.uint64)
+    batch_stale = []
+    zeros_tok = np.zeros(T_mb, np.float32)
+    for m in range(M):
+        ss = slice(m * S, (m + 1) * S)
+        mb = seam.MicroBatch(np.full(S, Ls), np.zeros(T_mb, np.int32), zeros_tok, zeros_tok, rewards[ss], False,
+                             sample_ids=np.arange(m * S, (m + 1) * S) + 1, producer_versions=prod_ver[ss])
+        batch_stale.append(mb.staleness(v_t, hist))
+    stale_hist = {int(k): int(v) for k, v in enumerate(hist) if v}
     g = torch.Generator(device=dev).manual_seed(17)
     old = (-3.0 + 0.5 * torch.randn(T, device=dev, generator=g)).float()
     ref = (old + 0.1 * torch.randn(T, device=dev, generator=g)).float()
-    adv = torch.randn(M * S, device=dev, generator=g)
-    cu = torch.arange(0, T + 1, Ls, dtype=torch.int32, device=dev)
+    cu, _, _, _ = tm.varlen_meta(torch.full((n_seq,), Ls, dtype=torch.int32, device=dev), T=T, want=("cu",))
+    adv = tm.grpo_advantage(torch.from_numpy(rewards).to(dev), torch.from_numpy(gids).to(dev))  # G = 16
     adv_tok, w_tok = tm.token_weights(cu, adv, torch.from_numpy(mask).to(dev), T, _lib.NORM_EXPLICIT, 1.0 / n_act)
     params = _lib.default_loss_params(norm_mode=_lib.NORM_EXPLICIT, inv_norm=1.0 / n_act)
     dsh = torch.empty_like(shard)
@@ -366,9 +389,12 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     ach = by_min / (per_mb_ms / 1e3) / 1e9
     if rank == 0:
         _line(args, world, "tokens/s vocab-parallel fused logprob+GRPO loss fwd+bwd (Qwen3-4B vocab)",
-              T / (ms_step / 1e3), ms_step, "bf16",
-              {"workload": f"vocab-parallel P={P}: 4 x (32 x 4096 tok), shard V/P={Vp}, staleness-tagged samples",
-               "config_index": 5, "tokens_per_step": T, "vocab": V, "vocab_shard": Vp,
+              n_act / (ms_step / 1e3), ms_step, "bf16",
+              {"workload": f"vocab-parallel P={P}: 256 prompts x 16 rollouts x {Ls} tok ({M} micro-batches of "
+                           f"{S} seqs), GRPO G=16, shard V/P={Vp}, staleness-tagged samples",
+               "config_index": 5, "tokens_per_step": T, "loss_active_tokens_per_step": n_act,
+               "value_counts": "loss-active tokens", "value_all_tokens": T / (ms_step / 1e3),
+               "vocab": V, "vocab_shard": Vp, "batch_staleness_max": int(max(batch_stale)),
                "parallelism": (f"vocab-parallel tp{P} (" + ("in-kernel peer-mailbox exchange over NVLink, 32 B/row/peer"
                                                              if fused else "NCCL all-gather 16 B/token/rank") + ")"),
                "_scaling": "strong",

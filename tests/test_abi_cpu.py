@@ -106,3 +106,25 @@ def test_product_package_never_touches_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", '#include "sf_oracle', "libsf_oracle", "oracle/_build"):
                     assert bad not in txt, (f, bad)
+
+
+def test_seam_library_exports_every_header_function():
+    """libsf_seam.so (the C++ trainer seam behind a C-ABI) exports every
+    function include/staleflow/train_math_seam_c.h declares; a batch encodes
+    without a GPU."""
+    import numpy as np
+
+    from paper_2604_11554_b200 import seam
+
+    names = seam.header_functions()
+    l = seam.lib()
+    assert names and not [n for n in names if not hasattr(l, n)]
+    assert set(seam._SIGS) <= set(names)
+    b = seam.MicroBatch([3, 2], np.arange(5), np.zeros(5), np.zeros(5), [0.5, -0.5], True,
+                        loss_mask=np.ones(5, np.uint8))
+    assert b.T == 5 and b.B == 2
+    import torch
+
+    if not torch.cuda.is_available():  # no device: the seam reports Internal, it does not crash
+        s = ctypes.c_void_p()
+        assert l.sf_seam_create(0, ctypes.byref(s)) == _lib.INTERNAL

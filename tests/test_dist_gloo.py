@@ -75,7 +75,36 @@ def _work(rank, world, q):
     ref, _, _, _, _ = orc.pg_loss_fwd_bwd(full["logits"], full["targets"], full["old"], full["ref"], adv, w,
                                           want_dlogits=False)
     ok_dp = bool(np.allclose(t.numpy(), ref, rtol=1e-12, atol=1e-15))
-    q.put((rank, ok_vp, ok_dp))
+    # ---- sequence sharding with UNEQUAL per-rank masks: the DAPO token-mean is
+    # over the global batch, so every rank weights by 1 / (sum of all ranks'
+    # active tokens) (data_parallel.global_inv_norm), not 1 / its own count
+    from paper_2604_11554_b200 import data_parallel as dp
+
+    full2 = orc.synth_problem(13, [6, 9, 7, 12], 512, "bf16", prompt_max=0)
+    cu2 = np.concatenate([[0], np.cumsum(full2["lens"])])
+    mask = np.ones(full2["T"], np.uint8)
+    plen = [1, 5, 0, 3]  # ranks end up with 9+? active tokens each, unequal
+    for s_ in range(4):
+        mask[cu2[s_]:cu2[s_] + plen[s_]] = 0
+    adv2 = np.linspace(-1, 1, full2["T"]).astype(np.float32)
+    mine2 = np.arange(cu2[2 * rank], cu2[2 * rank + 2])
+    local_active = int(mask[mine2].sum())
+    inv = dp.global_inv_norm(local_active)
+    w_loc = (mask[mine2] * inv).astype(np.float32)
+    met2, _, _, _, _ = orc.pg_loss_fwd_bwd(full2["logits"][mine2], full2["targets"][mine2], full2["old"][mine2],
+                                           full2["ref"][mine2], adv2[mine2], w_loc, want_dlogits=False)
+    t2 = dp.reduce_step_metrics(torch.from_numpy(met2))
+    w_all = (mask / mask.sum()).astype(np.float32)
+    ref2, _, _, _, _ = orc.pg_loss_fwd_bwd(full2["logits"], full2["targets"], full2["old"], full2["ref"], adv2, w_all,
+                                           want_dlogits=False)
+    ok_dp2 = bool(np.allclose(t2.numpy(), ref2, rtol=1e-6, atol=1e-12))
+    # the per-rank normaliser (round 1's bench) would not be the global token-mean
+    w_bad = (mask[mine2] / max(local_active, 1)).astype(np.float32)
+    met3, _, _, _, _ = orc.pg_loss_fwd_bwd(full2["logits"][mine2], full2["targets"][mine2], full2["old"][mine2],
+                                           full2["ref"][mine2], adv2[mine2], w_bad, want_dlogits=False)
+    t3 = dp.reduce_step_metrics(torch.from_numpy(met3))
+    ok_dp2 = ok_dp2 and not np.allclose(t3.numpy()[5], ref2[5], rtol=1e-3)  # ratio ~ world x the mean
+    q.put((rank, ok_vp, ok_dp and ok_dp2))
 
 
 def test_two_rank_gloo_protocols():
