@@ -68,20 +68,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
-// Wait for a phase that is usually far off, without the suspend-and-probe loop
-// of mbar_wait: a warp that is ahead of its producer by design (backward
-// warps waiting for a row's scalars, control warps for the partials) would
-// otherwise wake on every mbarrier event of the CTA and re-issue its probe,
-// taking issue slots from the warps on the critical path. ns = 0 keeps the
-// hardware-suspended form.
-__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity, uint32_t ns) {
-  if (ns == 0) {
-    mbar_wait(bar, parity);
-    return;
-  }
-  while (!mbar_test(bar, parity)) __nanosleep(ns);
-}
-
 // Wait with cluster-scope acquire: pairs with remote release-arrives from peer
 // CTAs of the cluster (DSMEM mailbox exchange).
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
@@ -287,21 +273,6 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t u) {
   return __uint_as_float(static_cast<uint32_t>(u) << 16);
 }
 
-// fp16x2 pack (round to nearest) and unpack: the row store of the e-store
-// loss kernel keeps 2^(z*log2e - base) as fp16 (11 significant bits).
-__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-__device__ __forceinline__ float2 unpack_f16x2(uint32_t u) {
-  float lo, hi;
-  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-      : "=f"(lo), "=f"(hi)
-      : "r"(u));
-  return make_float2(lo, hi);
-}
-
 // Round-to-nearest-even pack of two fp32 into bf16x2 (lo in the low half).
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
@@ -351,10 +322,15 @@ __device__ __forceinline__ Stats stats_merge(Stats a, Stats b) {
 // it once (one ex2) and s, w are summed — 15 shuffles and 1 ex2 per lane
 // instead of 5 pairwise merges with 2 ex2 each. Fixed butterfly order, so the
 // result is deterministic.
+__device__ __forceinline__ float warp_max_f32(float v) {
+  // sm_100a: one CREDUX.MAX.F32 instead of a 5-level shuffle/max chain
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 __device__ __forceinline__ Stats warp_merge(Stats v) {
-  float M = v.m2;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float M = warp_max_f32(v.m2);
   float s = 0.f, w = 0.f;
   if (v.m2 != -INFINITY) {
     const float d = v.m2 - M;

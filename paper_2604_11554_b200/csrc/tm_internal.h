@@ -51,9 +51,6 @@ struct RowArgs {
   int* xp_abort = nullptr;  // device: first CTA to time out tells the others to stop waiting
   unsigned long long xp_timeout_ns = 300000000000ull;  // SF_TM_XP_TIMEOUT_S (default 300 s)
   int xp_grid = 0;          // > 0: cap the exchange grid (emulated ranks sharing one GPU)
-  // back-off sleeps (ns) of the waits that are off the critical path: the
-  // backward's per-row scalars and the control warps' per-row partials
-  unsigned sleep_bwd_ns = 0, sleep_ctl_ns = 0;
   // optional wait-time instrumentation (debug only): per-role clock64 sums
   unsigned long long* dbg = nullptr;
   // workspace (owned by the handle)

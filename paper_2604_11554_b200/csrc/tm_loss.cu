@@ -99,11 +99,6 @@ struct RowScal {
   uint32_t town;   // (thread owning the target << 8) | its element index j
 };
 constexpr int kMaxChunks = kStore - 2;      // a whole row slice must fit the row store
-// E-store (ES) rows: a chunk whose exponentials sum past this (relative to the
-// warp's current base) moves the base up, so every stored e = 2^(z*log2e -
-// base) is <= 2^11 and the fp16 row-store words cannot overflow; the values
-// that matter for p (>= 2^-18 of the row maximum) stay >= 2^-18 in fp16.
-constexpr float kEsMax = 2048.f;
 
 template <typename T>
 struct Geo {
@@ -231,7 +226,7 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // the boundary dlogits vectors are stored per element. Reads extend to whole
 // 16-B sectors inside the tensor; the very last row's tail sector is filled by
 // the producer with element loads instead, so nothing past the tensor is read.
-template <typename T, int C, bool XP = false, bool UA = false, bool ES = false>
+template <typename T, int C, bool XP = false, bool UA = false>
 __global__ void __launch_bounds__(kThreads, 1)
     loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
@@ -255,9 +250,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t rcv_done[kCredD];  // XP: receiver progress (sender credit)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t sink_sh[kBW];
-  // ES: exponent base of each row-store slot's chunk, per forward warp, indexed
-  // by the slot's use parity (the next write of an entry is two uses later)
-  __shared__ float cbase[ES ? 2 : 1][ES ? kStore : 1][kFW];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -319,6 +311,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       (void)t;
       return 0;
     }
+  };
+  // A partial chunk (the front / tail of a row slice) may hold no element of a
+  // whole warp's share (a narrow vocab-parallel shard row ends a few vectors
+  // into its last chunk). Such a warp keeps the barrier protocol (waits and
+  // arrives, so every phase count stays exact) but skips the loads, the row
+  // store and the math. The test is warp-uniform and the forward warp and its
+  // backward partner (same element mapping) take the same decision.
+  auto warp_idle = [&](int k, bool partial, int mis, int span, int wbase) -> bool {
+    if (!partial) return false;
+    const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+    const int a0 = EV * wbase, a1 = EV * (wbase + 32);  // the warp's first-vector block
+    const int b0 = G::HALF + a0, b1 = G::HALF + a1;     // ... and second-vector block
+    return !(a0 < rem && a1 > lo) && !(b0 < rem && b1 > lo);
   };
   // where the backward finds the target column (computed once per row by the
   // control warp): chunk, owning thread and its element index
@@ -429,15 +434,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float2 w2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const uint32_t ts0 = ts;
-      const uint32_t tph0 = tph;
-      bool nobase = false;  // ES: this warp's share of chunk 0 held nothing finite
-      (void)tph0;
-
       // One chunk: smem -> registers (slot released at once) -> TMEM stash ->
       // online softmax. `first` sets the exponent base from this thread's max of
       // chunk 0; `partial` masks elements past the slice end. Both are constants
       // at every call site, so the hot loop carries no per-chunk branches.
-      auto chunk_raw = [&](int k, bool first, bool partial) {
+      auto chunk = [&](int k, bool first, bool partial) {
+        if (warp_idle(k, partial, mis, span, 32 * fw)) {
+          DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
+          mbar_arrive(empty0 + 8u * slot);  // nothing read from the slot
+          if (++slot == kSlots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+          DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
+          if (first) m2 = 0.f;  // no element of this warp in the row's only chunk
+          mbar_arrive(tfull0 + 8u * ts);  // nothing written to the row-store slot
+          if (++ts == kStore) {
+            ts = 0;
+            tph ^= 1u;
+          }
+          return;
+        }
         DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
         const uint32_t sa = ring_t + slot * kCB;
         uint4 v0 = lds128(sa);
@@ -545,148 +562,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           tph ^= 1u;
         }
       };
-
-      // ES (e-store) chunk: the row store receives e = 2^(z*log2e - base) instead
-      // of the raw logits, so the backward forms p * |c0| with one multiply by
-      // 2^(base - lse2f) per chunk instead of one exponential per element. The
-      // base is warp-uniform (the warp's maximum of chunk 0), moved up when a
-      // chunk's exponentials sum past kEsMax; each slot's base goes to cbase.
-      // bf16 rows store e as fp16 (11 significant bits: the bf16 dlogits stay
-      // within 1 ulp), fp32 rows store fp32 e.
-      auto chunk_es = [&](int k, bool first, bool partial) {
-        DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
-        const uint32_t sa = ring_t + slot * kCB;
-        const int rem = span - k * CE;             // valid elements end here (chunk coordinates)
-        const int lo = (UA && k == 0) ? mis : 0;   // ... and start here
-        // the warp's maximum of this chunk's valid elements (x * c)
-        auto chunk_max = [&](uint4 v0, uint4 v1) {
-          float x[NE];
-          unpack(logits, v0, v1, x);
-          float xm = -INFINITY;
-#pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const int pj = elem_off<T>(ftid, j);
-            if (!partial || (pj >= lo && pj < rem)) xm = fmaxf(xm, x[j]);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
-          return xm * c;
-        };
-        if (first) {
-          m2 = chunk_max(lds128(sa), lds128(sa + kCB / 2));
-          if (!(m2 > -INFINITY)) {  // nothing finite: provisional base, repaired at row end
-            m2 = 0.f;
-            nobase = true;
-          }
-        }
-        // exponentials of the chunk against the current base, straight into the
-        // row-store words (invalid positions 0) and the chunk's partial sums
-        uint32_t q[8];
-        float2 cs[2], cw[2];
-        auto expo = [&](uint4 v0, uint4 v1) {
-          float x[NE];
-          unpack(logits, v0, v1, x);
-          cs[0] = cs[1] = cw[0] = cw[1] = make_float2(0.f, 0.f);
-          const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int p0 = v * G::HALF + EV * ftid;
-            const bool whole = !partial || (p0 >= lo && p0 + EV <= rem);
-            float ev[EV];
-            if (whole) {
-#pragma unroll
-              for (int h = 0; h < EV / 2; ++h) {
-                const int p = v * (EV / 2) + h;
-                const float2 av = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]), c2, nm2);
-                const float2 e2 = make_float2(ex2(av.x), ex2(av.y));
-                cs[h & 1] = __fadd2_rn(cs[h & 1], e2);
-                cw[h & 1] = __ffma2_rn(e2, av, cw[h & 1]);
-                ev[2 * h] = e2.x;
-                ev[2 * h + 1] = e2.y;
-              }
-            } else {
-              // boundary vector of an unaligned row (element masks), or a vector
-              // past the end of an aligned slice (all masked)
-#pragma unroll
-              for (int j = 0; j < EV; ++j) {
-                const int pj = p0 + j;
-                ev[j] = 0.f;
-                if (UA && pj >= lo && pj < rem && x[v * EV + j] != -INFINITY) {
-                  const float av = fmaf(x[v * EV + j], c, -m2);
-                  ev[j] = ex2(av);
-                  cs[0].x += ev[j];
-                  cw[0].x = fmaf(ev[j], av, cw[0].x);
-                }
-              }
-            }
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              if constexpr (sizeof(T) == 2) {
-                q[4 * v + h] = pack_f16x2(ev[2 * h], ev[2 * h + 1]);
-              } else {
-                q[4 * v + h] = __float_as_uint(ev[h]);
-              }
-            }
-          }
-        };
-        expo(lds128(sa), lds128(sa + kCB / 2));
-        {
-          const float2 c01 = __fadd2_rn(cs[0], cs[1]);
-          if (__any_sync(0xffffffffu, !(c01.x + c01.y <= kEsMax))) {
-            // rare: this chunk rises far above the base. New base = the warp's
-            // maximum of this chunk; rescale the running sums, redo the chunk
-            // (re-read from the ring slot, which is still held).
-            const uint4 r0 = lds128(sa), r1 = lds128(sa + kCB / 2);
-            const float nb = fmaxf(m2, chunk_max(r0, r1));
-            const float d = m2 - nb, f = ex2(d);
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              w2[i] = make_float2(f * fmaf(s2[i].x, d, w2[i].x), f * fmaf(s2[i].y, d, w2[i].y));
-              s2[i] = make_float2(s2[i].x * f, s2[i].y * f);
-            }
-            m2 = nb;
-            expo(r0, r1);
-          }
-        }
-        s2[0] = __fadd2_rn(s2[0], cs[0]);
-        s2[1] = __fadd2_rn(s2[1], cs[1]);
-        w2[0] = __fadd2_rn(w2[0], cw[0]);
-        w2[1] = __fadd2_rn(w2[1], cw[1]);
-        uint4 q0 = make_uint4(q[0], q[1], q[2], q[3]), q1 = make_uint4(q[4], q[5], q[6], q[7]);
-        DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
-        const bool in_tmem = ts < kTSlots;
-        if (in_tmem) {
-          tc_fence_after();
-          tmem_st8(tm_t + ts * static_cast<uint32_t>(kSlotCols), q0, q1);
-        } else {
-          const uint32_t sa2 = stash_t + (ts - kTSlots) * kCB;
-          sts128(sa2, q0);
-          sts128(sa2 + kCB / 2, q1);
-        }
-        // the row-store words were computed from the slot's LDS: they have returned
-        mbar_arrive(empty0 + 8u * slot);
-        if (++slot == kSlots) {
-          slot = 0;
-          ph ^= 1u;
-        }
-        if (lane == 0) cbase[tph & (ES ? 1u : 0u)][ES ? ts : 0][fw] = m2;
-        if (in_tmem) {
-          tmem_wait_st();
-          tc_fence_before();
-        }
-        mbar_arrive(tfull0 + 8u * ts);  // release: orders the smem stores (and cbase) too
-        if (++ts == kStore) {
-          ts = 0;
-          tph ^= 1u;
-        }
-      };
-      auto chunk = [&](int k, bool first, bool partial) {
-        if constexpr (ES) {
-          chunk_es(k, first, partial);
-        } else {
-          chunk_raw(k, first, partial);
-        }
-      };
       if constexpr (UA) {
         // peeled like the aligned schedule: only the front and tail chunks are masked
         const int nfull_r = span / CE;
@@ -712,77 +587,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Repair (rare): a -inf logit (0 * -inf in w) or an exponent overflow
       // (a logit > 126/log2e above the chunk-0 base) made s or w non-finite:
       // recompute this thread's partials exactly from its TMEM words.
-      if constexpr (ES) {
-        // Repair (rare): a -inf logit (0 * -inf in w) or a warp share whose
-        // chunk 0 held nothing finite. The row store holds exponentials, not
-        // logits: re-read this warp's elements of the row from HBM (the row's
-        // dlogits are not written yet, so in-place rows are intact), rebase on
-        // the warp's true maximum and rewrite the row store and its bases.
-        const bool bad_es = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f) || nobase;
-        if (__any_sync(0xffffffffu, bad_es)) {
-          const T* rowg = logits + t * a.ld + slice_start - mis;
-          float mx = -INFINITY;
-          for (int k = 0; k < nck_r; ++k) {
-            const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
-#pragma unroll
-            for (int j = 0; j < NE; ++j) {
-              const int pj = elem_off<T>(ftid, j);
-              if (pj >= lo && pj < rem) mx = fmaxf(mx, ldg_elem(rowg, static_cast<int64_t>(k) * CE + pj));
-            }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          const float mb2 = (mx > -INFINITY) ? mx * c : 0.f;
-          float sr = 0.f, wr = 0.f;
-          uint32_t q = ts0, qp = tph0;
-          for (int k = 0; k < nck_r; ++k) {
-            const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
-            float e[NE];
-#pragma unroll
-            for (int j = 0; j < NE; ++j) {
-              const int pj = elem_off<T>(ftid, j);
-              e[j] = 0.f;
-              if (pj >= lo && pj < rem) {
-                const float xv = ldg_elem(rowg, static_cast<int64_t>(k) * CE + pj);
-                if (xv != -INFINITY) {
-                  const float av = fmaf(xv, c, -mb2);
-                  e[j] = ex2(av);
-                  sr += e[j];
-                  wr = fmaf(e[j], av, wr);
-                }
-              }
-            }
-            uint4 q0, q1;
-            if constexpr (sizeof(T) == 2) {
-              q0 = make_uint4(pack_f16x2(e[0], e[1]), pack_f16x2(e[2], e[3]), pack_f16x2(e[4], e[5]),
-                              pack_f16x2(e[6], e[7]));
-              q1 = make_uint4(pack_f16x2(e[8], e[9]), pack_f16x2(e[10], e[11]), pack_f16x2(e[12], e[13]),
-                              pack_f16x2(e[14], e[15]));
-            } else {
-              q0 = make_uint4(__float_as_uint(e[0]), __float_as_uint(e[1]), __float_as_uint(e[2]),
-                              __float_as_uint(e[3]));
-              q1 = make_uint4(__float_as_uint(e[4]), __float_as_uint(e[5]), __float_as_uint(e[6]),
-                              __float_as_uint(e[7]));
-            }
-            if (q < static_cast<uint32_t>(kTSlots)) {
-              tmem_st8(tm_t + q * static_cast<uint32_t>(kSlotCols), q0, q1);
-            } else {
-              sts128(stash_t + (q - kTSlots) * kCB, q0);
-              sts128(stash_t + (q - kTSlots) * kCB + kCB / 2, q1);
-            }
-            if (lane == 0) cbase[qp & (ES ? 1u : 0u)][ES ? q : 0][fw] = mb2;
-            if (++q == kStore) {
-              q = 0;
-              qp ^= 1u;
-            }
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          __threadfence_block();  // order every lane's rewrite before lane 0's release below
-          __syncwarp();
-          my = Stats{mb2, sr, wr};
-        }
-      } else {
       const bool bad = !(fabsf(my.s) <= 3.0e38f) || !(fabsf(my.w) <= 3.0e38f);
       if (__any_sync(0xffffffffu, bad)) {
         float mx = -INFINITY;
@@ -823,7 +627,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (bad) my = Stats{mb2, sr, wr};
       }
-      }  // ES / raw repair
       if (my.s == 0.f) my = stats_empty();  // nothing finite in this thread's share
       // Per-warp partial -> smem ring; no CTA barrier: the control warp
       // merges the 12 partials, so forward warps go straight to the next row.
@@ -902,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t m = nrow - kXpCredit;
             mbar_wait(smem_u32(&rcv_done[m % kCredD]), (m / kCredD) & 1u);
           }
-          DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u, a.sleep_ctl_ns));
+          DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u));
           Stats v = stats_empty();
           if (lane < kFW) {
             const float4 r = red[rs][lane];
@@ -1030,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // of the row (in-place dlogits stays safe)
       float zy = __int_as_float(0x7fc00000);
       if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
-      DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&red_bar[rs]), rpar, a.sleep_ctl_ns));
+      DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), rpar));
       Stats v = stats_empty();
       if (lane < kFW) {
         const float4 r = red[rs][lane];
@@ -1152,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nck_r = UA ? (span + CE - 1) / CE : nck;
       const uint32_t rs = nrow % kRD;
       const uint32_t rpar = (nrow / kRD) & 1u;
-      DBG_WAIT(w_a, mbar_wait_backoff(smem_u32(&scal_bar[rs]), rpar, a.sleep_bwd_ns));
+      DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
       const RowScal rsc = scal[rs];
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
@@ -1166,6 +969,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // into the exponent and the sign applied to the packed words, 1 = no
       // entropy term, 2 = entropy term. `partial` masks past the slice end.
       auto bchunk = [&](int k, bool partial, int mode) {
+        if (warp_idle(k, partial, mis, span, 32 * bw)) {
+          DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
+          mbar_arrive(tempty0 + 8u * ts);  // nothing read from the row-store slot
+          if (++ts == kStore) {
+            ts = 0;
+            tph ^= 1u;
+          }
+          return;
+        }
         DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
         tc_fence_after();
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
@@ -1335,105 +1147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (late) mbar_arrive(rel);
       };
-      // ES chunk: e = 2^(z*log2e - base) from the row store (fp16 for bf16 rows,
-      // fp32 for fp32 rows); dlogits = gt*[v == y] - c0*p = e * f (+ gt), with
-      // f = -sign(c0) * 2^(base - lse2f) once per chunk (lse2f folds log2|c0|).
-      auto bchunk_es = [&](int k, bool partial) {
-        DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
-        tc_fence_after();
-        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
-        // this slot's base: the forward rewrites this entry two uses of the slot
-        // later, so reading it here cannot race the early TMEM-slot release
-        const float base = cbase[tph & (ES ? 1u : 0u)][ES ? ts : 0][bw];
-        const uint32_t rel = tempty0 + 8u * ts;
-        const bool late = ts >= kTSlots;
-        if (!late) {
-          tmem_ld8(tm_t + ts * static_cast<uint32_t>(kSlotCols), w0, w1);
-          tmem_wait_ld(w0, w1);
-          tc_fence_before();
-          mbar_arrive(rel);
-        } else {
-          w0 = lds128(stash_t + (ts - kTSlots) * kCB);
-          w1 = lds128(stash_t + (ts - kTSlots) * kCB + kCB / 2);
-        }
-        if (++ts == kStore) {
-          ts = 0;
-          tph ^= 1u;
-        }
-        const float fm = ex2(base - lse2f);
-        const float f = neg ? -fm : fm;
-        const float2 f2 = make_float2(f, f);
-        float gr[NE];
-        if constexpr (sizeof(T) == 2) {
-          const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-          for (int p = 0; p < 8; ++p) {
-            const float2 g2 = __fmul2_rn(unpack_f16x2(wd[p]), f2);
-            gr[2 * p] = g2.x;
-            gr[2 * p + 1] = g2.y;
-          }
-        } else {
-          const float2 g0 = __fmul2_rn(make_float2(__uint_as_float(w0.x), __uint_as_float(w0.y)), f2);
-          const float2 g1 = __fmul2_rn(make_float2(__uint_as_float(w0.z), __uint_as_float(w0.w)), f2);
-          const float2 g2 = __fmul2_rn(make_float2(__uint_as_float(w1.x), __uint_as_float(w1.y)), f2);
-          const float2 g3 = __fmul2_rn(make_float2(__uint_as_float(w1.z), __uint_as_float(w1.w)), f2);
-          gr[0] = g0.x; gr[1] = g0.y; gr[2] = g1.x; gr[3] = g1.y;
-          gr[4] = g2.x; gr[5] = g2.y; gr[6] = g3.x; gr[7] = g3.y;
-        }
-        if (k == ck) {
-#pragma unroll
-          for (int j = 0; j < NE; ++j)
-            if (j == jt) gr[j] += gt;
-        }
-        T* dst = drow + k * CE;
-        const int rem = span - k * CE;
-        const uint32_t dep = w0.x ^ w1.w ^ __float_as_uint(f);
-        if (!partial) {
-          store_vec(dst + EV * btid, gr);
-          store_vec(dst + G::HALF + EV * btid, gr + EV);
-        } else if (UA) {
-          const int lo = (k == 0) ? mis : 0;
-          bool any = false;
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int p0 = v * G::HALF + EV * btid;
-            if (p0 >= lo && p0 + EV <= rem) {
-              store_vec(dst + p0, gr + v * EV);
-              any = true;
-            } else {
-#pragma unroll
-              for (int j = 0; j < EV; ++j)
-                if (p0 + j >= lo && p0 + j < rem) {
-                  st1(dst + p0 + j, gr[v * EV + j]);
-                  any = true;
-                }
-            }
-          }
-          if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
-        } else {
-          // vector-granular tail; a thread storing nothing still orders its
-          // loads before the release through a dependent (dummy) smem store
-          const bool s0 = EV * btid < rem;
-          if (s0) store_vec(dst + EV * btid, gr);
-          if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
-          if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
-        }
-        if (late) mbar_arrive(rel);
-      };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
-      if constexpr (ES) {
-        const int nfull_r = UA ? span / CE : nfull;
-        const bool front = UA && (mis > 0 || span < CE);
-        if (nck_r > 0) {
-          if (front || nfull_r == 0) {
-            bchunk_es(0, true);
-          } else {
-            bchunk_es(0, false);
-          }
-          for (int k = 1; k < nfull_r; ++k) bchunk_es(k, false);
-          if (nck_r > nfull_r && nck_r > 1) bchunk_es(nck_r - 1, true);
-        }
-      } else if constexpr (UA) {
+      if constexpr (UA) {
         const int nfull_r = span / CE;
         const bool front = mis > 0 || span < CE;
         auto sched = [&](auto md) {
@@ -1490,9 +1205,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
-template <typename T, int C, bool XP = false, bool UA = false, bool ES = false>
+template <typename T, int C, bool XP = false, bool UA = false>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  auto kern = loss_tmem_kernel<T, C, XP, UA, ES>;
+  auto kern = loss_tmem_kernel<T, C, XP, UA>;
   static PerDevice cache;  // per instantiation and device
   int& max_active = cache();
   {
@@ -1534,11 +1249,6 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   }
   RowArgs ad = a;
   ad.dbg = debug_counters();
-  static const unsigned sleeps[2] = {
-      [] { const char* v = getenv("SFTM_SLEEP_BWD"); return v ? static_cast<unsigned>(atoi(v)) : 0u; }(),
-      [] { const char* v = getenv("SFTM_SLEEP_CTL"); return v ? static_cast<unsigned>(atoi(v)) : 0u; }()};
-  ad.sleep_bwd_ns = sleeps[0];
-  ad.sleep_ctl_ns = sleeps[1];
   if (ncl > a.max_partial_blocks) ncl = a.max_partial_blocks;
   if (ncl < 1) ncl = 1;
   cudaLaunchConfig_t cfg = {};
@@ -1567,38 +1277,19 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   return e;
 }
 
-// The e-store schedule can take every row whose gradient has no entropy term
-// (entropy_coef == 0, the DAPO default): the backward then needs p*c0 only.
-// Measured on B200: half the MUFU work and ~180 MHz more SM
-// clock under the power cap, but the forward warps become the critical role
-// and the throughput is 0.5% below the raw-logit store, so it is opt-in
-// (SFTM_ES=1) until the forward/backward warp split is rebalanced.
-inline bool use_es(const RowArgs& a) {
-  static const bool on = [] {
-    const char* v = getenv("SFTM_ES");
-    return v && v[0] == '1';
-  }();
-  return on && a.ent_coef == 0.f;
-}
-
-template <typename T, bool ES>
-int launch_with_es(const RowArgs& a, int C, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  switch (C) {
-    case 1: return launch_c<T, 1, false, false, ES>(a, slice, s, info);
-    case 2: return launch_c<T, 2, false, false, ES>(a, slice, s, info);
-    case 3: return launch_c<T, 3, false, false, ES>(a, slice, s, info);
-    case 4: return launch_c<T, 4, false, false, ES>(a, slice, s, info);
-    case 8: return launch_c<T, 8, false, false, ES>(a, slice, s, info);
-  }
-  return -2;
-}
-
 template <typename T>
 int launch_with(const RowArgs& a, int C, cudaStream_t s, LaunchInfo* info) {
   using G = Geo<T>;
   int64_t slice = (a.V + C - 1) / C;
   slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
-  return use_es(a) ? launch_with_es<T, true>(a, C, slice, s, info) : launch_with_es<T, false>(a, C, slice, s, info);
+  switch (C) {
+    case 1: return launch_c<T, 1>(a, slice, s, info);
+    case 2: return launch_c<T, 2>(a, slice, s, info);
+    case 3: return launch_c<T, 3>(a, slice, s, info);
+    case 4: return launch_c<T, 4>(a, slice, s, info);
+    case 8: return launch_c<T, 8>(a, slice, s, info);
+  }
+  return -2;
 }
 
 template <typename T>
@@ -1614,8 +1305,7 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
   if (ua) {
     if ((a.V + G::EV - 1 + G::CE - 1) / G::CE > kMaxChunks) return -2;
-    return use_es(a) ? launch_c<T, 1, false, true, true>(a, a.V, s, info)
-                     : launch_c<T, 1, false, true, false>(a, a.V, s, info);
+    return launch_c<T, 1, false, true>(a, a.V, s, info);
   }
   static const int forced = [] {  // tuning knob: SFTM_LOSS_C=1|2|3|4|8
     const char* v = getenv("SFTM_LOSS_C");
@@ -1654,8 +1344,7 @@ int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
     using G = loss::Geo<T>;
     int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
     if ((slice + G::CE - 1) / G::CE > loss::kMaxChunks) return -2;
-    return loss::use_es(a) ? loss::launch_c<T, 1, true, false, true>(a, slice, s, info)
-                           : loss::launch_c<T, 1, true, false, false>(a, slice, s, info);
+    return loss::launch_c<T, 1, true>(a, slice, s, info);
   };
   if (a.dtype == 1) return go(uint16_t{});
   return go(float{});

@@ -528,13 +528,21 @@ int bench(int micro_batches) {
   CU(cudaEventRecord(e0, nullptr));
   int n = 0;
   uint64_t tokens = 0;
+  double fetch_ms = 0, step_ms = 0;
+  std::vector<MicroBatch> kept;
   for (int i = 1; i < micro_batches; ++i) {
+    const auto a0 = std::chrono::steady_clock::now();
     auto got = loader.next_micro_batch();
     if (!got.ok()) break;
+    const auto a1 = std::chrono::steady_clock::now();
     CHECK(actor.step(got.value(), d_logits, SF_TM_BF16, c.V, d_dl, prm, met.data() + i * SF_TM_NUM_METRICS,
                      nullptr, c.G) == SF_TM_OK);
+    const auto a2 = std::chrono::steady_clock::now();
     CHECK(loader.ack(got.value()).ok());
+    fetch_ms += std::chrono::duration<double, std::milli>(a1 - a0).count();
+    step_ms += std::chrono::duration<double, std::milli>(a2 - a1).count();
     tokens += static_cast<uint64_t>(actor.packed().T);
+    kept.push_back(got.value());
     ++n;
   }
   CU(cudaEventRecord(e1, nullptr));
@@ -543,11 +551,33 @@ int bench(int micro_batches) {
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e0, e1));
   const double wall = std::chrono::duration<double, std::milli>(h1 - h0).count();
+  // the same steps on the already fetched batches (no bus in the timed region)
+  CU(cudaEventRecord(e0, nullptr));
+  for (int i = 0; i < n; ++i)
+    CHECK(actor.step(kept[i], d_logits, SF_TM_BF16, c.V, d_dl, prm, met.data(), nullptr, c.G) == SF_TM_OK);
+  CU(cudaEventRecord(e1, nullptr));
+  CU(cudaEventSynchronize(e1));
+  float ms_steps = 0;
+  CU(cudaEventElapsedTime(&ms_steps, e0, e1));
+  // and the fused loss alone on device-resident fields
+  CU(cudaEventRecord(e0, nullptr));
+  for (int i = 0; i < n; ++i)
+    CHECK(sf_tm_pg_step_host(h, d_logits, SF_TM_BF16, actor.packed().T, c.V, c.V, actor.packed().targets.data(),
+                             actor.packed().logp.data(), actor.packed().ref_logp.data(), nullptr,
+                             actor.packed().seq_lens.data(), nullptr, actor.packed().per_sample.data(),
+                             actor.packed().group_ids.data(), actor.packed().B, -1.f, SF_TM_STD_UNBIASED, &prm, d_dl,
+                             c.V, met.data(), nullptr) == SF_TM_OK);
+  CU(cudaEventRecord(e1, nullptr));
+  CU(cudaEventSynchronize(e1));
+  float ms_abi = 0;
+  CU(cudaEventElapsedTime(&ms_abi, e0, e1));
   std::printf("{\"path\": \"StreamLoader::next_micro_batch -> ActorLossSeam::step (reference bus, in-process)\", "
               "\"micro_batches\": %d, \"tokens\": %llu, \"ms_per_micro_batch\": %.4f, \"tokens_per_s\": %.1f, "
-              "\"wall_ms_per_micro_batch\": %.4f, \"bus_bytes\": %llu}\n",
-              n, static_cast<unsigned long long>(tokens), ms / n, tokens / (ms / 1e3), wall / n,
-              static_cast<unsigned long long>(loader.wait_stats().bus_bytes));
+              "\"wall_ms_per_micro_batch\": %.4f, \"host_fetch_ms_per_micro_batch\": %.4f, "
+              "\"host_step_call_ms_per_micro_batch\": %.4f, \"seam_steps_only_ms_per_micro_batch\": %.4f, "
+              "\"c_abi_host_call_ms_per_micro_batch\": %.4f, \"bus_bytes\": %llu}\n",
+              n, static_cast<unsigned long long>(tokens), ms / n, tokens / (ms / 1e3), wall / n, fetch_ms / n,
+              step_ms / n, ms_steps / n, ms_abi / n, static_cast<unsigned long long>(loader.wait_stats().bus_bytes));
   cudaFree(d_logits);
   cudaFree(d_dl);
   sf_tm_destroy(h);

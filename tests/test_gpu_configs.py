@@ -266,3 +266,105 @@ def test_r3_record_token_to_layer_major_bit_exact(tm, orc, T, L, k, dt):
         w1, i1, m1 = tm.r3_gate_fwd(z, out)
         w2, i2, m2 = tm.r3_gate_fwd(z, torch.from_numpy(host).cuda())
         assert torch.equal(w1, w2) and torch.equal(i1, i2) and torch.equal(m1, m2)
+
+
+# ---------------------------------------------------------------------------- argument checks / bounds
+def test_pg_step_host_rejects_bad_dlogits_stride(tm, orc):
+    """the host seam call validates ld_d >= V and the in-place stride
+    like the device call (ConfigError before any copy is issued)."""
+    from paper_2604_11554_b200 import _lib
+
+    prob = orc.synth_problem(8, [6, 5], 4096, "bf16", prompt_max=2, G=2)
+    x = to_dev(prob)
+    pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()
+    args = [pin(prob["targets"], np.int32), pin(prob["old"], np.float32), pin(prob["ref"], np.float32),
+            pin(prob["lens"], np.int32), pin(prob["rewards"], np.float32), pin(prob["gids"], np.int32)]
+    narrow = torch.empty(prob["T"], 4000, dtype=torch.bfloat16, device="cuda")  # ld_d = 4000 < V
+    with pytest.raises(_lib.TrainMathError) as ex:
+        tm.pg_step_host(x, *args, dlogits=narrow)
+    assert ex.value.code == _lib.CONFIG_ERROR and "ld_d" in str(ex.value)
+    wide = torch.zeros(prob["T"], 4104, dtype=torch.bfloat16, device="cuda")
+    wide[:, :4096] = x
+    view = wide[:, :4096]
+    h = tm.handle(0)
+    params = _lib.default_loss_params()
+    met = torch.empty(_lib.NUM_METRICS).pin_memory()
+    # dlogits == logits but with another row stride: refused
+    rc = _lib.lib().sf_tm_pg_step_host(h.ptr, tm._p(view), _lib.BF16, prob["T"], 4096, 4104, tm._p(args[0]),
+                                       tm._p(args[1]), tm._p(args[2]), None, tm._p(args[3]), None, tm._p(args[4]),
+                                       tm._p(args[5]), len(prob["lens"]), 1e-6, 0, ctypes_byref(params),
+                                       tm._p(view), 4096, tm._p(met), tm._stream(0))
+    assert rc == _lib.CONFIG_ERROR
+
+
+def ctypes_byref(p):
+    import ctypes
+
+    return ctypes.byref(p)
+
+
+def test_kernels_write_nothing_outside_their_outputs(tm, orc):
+    """A bounds check in place of compute-sanitizer (closed on this pool): every
+    output buffer of every kernel family is allocated with sentinel guard
+    regions before and after (and guard columns around strided rows), and the
+    guards must be untouched after the call."""
+    from paper_2604_11554_b200 import _lib
+
+    G = 4096  # guard elements on each side
+
+    def guarded(n, dtype, fill):
+        buf = torch.full((n + 2 * G,), fill, dtype=dtype, device="cuda")
+        return buf, buf[G:G + n]
+
+    def check(buf, fill, what):
+        torch.cuda.synchronize()
+        assert torch.all(buf[:G] == fill) and torch.all(buf[-G:] == fill), f"{what}: write outside the output"
+
+    cases = [("bf16", 151936, [9, 4]), ("bf16", 262144, [3]), ("bf16", 50257, [7, 5]), ("f32", 32000, [6, 6]),
+             ("bf16", 18992, [40, 33])]
+    for dt, V, lens in cases:
+        prob = orc.synth_problem(V % 1000, lens, V, dt, prompt_max=3)
+        x = to_dev(prob)
+        T = prob["T"]
+        tdt = x.dtype
+        buf, dl = guarded(T * V, tdt, 7.0)
+        dl = dl.view(T, V)
+        cu, _, mask, _ = tm.varlen_meta(i32(prob["lens"]), i32(prob["plens"]), T=T, want=("cu", "mask"))
+        adv = tm.grpo_advantage(f32(prob["rewards"]), i32(prob["gids"]))
+        at, wt = tm.token_weights(cu, adv, mask, T)
+        mbuf, met = guarded(_lib.NUM_METRICS, torch.float32, -5.0)
+        lbuf, lp = guarded(T, torch.float32, -5.0)
+        ebuf, en = guarded(T, torch.float32, -5.0)
+        rc = _lib.lib().sf_tm_pg_loss_fwd_bwd(tm.handle(0).ptr, tm._p(x), _lib.BF16 if dt == "bf16" else _lib.F32, T, V,
+                                              V, tm._p(i32(prob["targets"])), tm._p(f32(prob["old"])),
+                                              tm._p(f32(prob["ref"])), tm._p(at), tm._p(wt),
+                                              ctypes_byref(_lib.default_loss_params()), tm._p(dl), V, tm._p(met),
+                                              tm._p(lp), tm._p(en), tm._stream(0))
+        assert rc == 0
+        for b_, f_, w_ in ((buf, 7.0, "dlogits"), (mbuf, -5.0, "metrics"), (lbuf, -5.0, "logp"), (ebuf, -5.0, "H")):
+            check(b_, f_, f"{w_} {dt} V={V}")
+        # forward-only outputs
+        for b_, f_ in ((lbuf, -5.0), (ebuf, -5.0)):
+            b_.fill_(f_)
+        rc = _lib.lib().sf_tm_logprob_fwd(tm.handle(0).ptr, tm._p(x), _lib.BF16 if dt == "bf16" else _lib.F32, T, V,
+                                          V, tm._p(i32(prob["targets"])), 1.0, tm._p(lp), tm._p(en), None,
+                                          tm._stream(0))
+        assert rc == 0
+        check(lbuf, -5.0, "fwd logp")
+        check(ebuf, -5.0, "fwd entropy")
+    # R3 outputs and the record transpose
+    L, T, E, k = 3, 301, 128, 8
+    z = torch.randn(L, T, E, device="cuda")
+    rec = torch.topk(z, k, dim=-1).indices.to(torch.uint8)
+    wbuf, w = guarded(L * T * k, torch.float32, -5.0)
+    ibuf, idx = guarded(L * T * k, torch.int32, -5)
+    mmb, mm = guarded(L + 1, torch.int32, -5)
+    tm.r3_gate_fwd(z, rec, out=(w.view(L, T, k), idx.view(L, T, k), mm))
+    for b_, f_, n_ in ((wbuf, -5.0, "r3 w"), (ibuf, -5, "r3 idx"), (mmb, -5, "r3 mismatch")):
+        check(b_, f_, n_)
+    dzb, dz = guarded(L * T * E, torch.float32, -5.0)
+    tm.r3_gate_bwd(z, rec, w.view(L, T, k), torch.randn(L, T, k, device="cuda"), out=dz.view(L, T, E))
+    check(dzb, -5.0, "r3 dz")
+    rb, r = guarded(L * T * k, torch.uint8, 201)
+    tm.r3_record_layer_major(rec.permute(1, 0, 2).contiguous(), out=r.view(L, T, k))
+    check(rb, 201, "record transpose")
