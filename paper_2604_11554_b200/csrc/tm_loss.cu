@@ -53,6 +53,10 @@ namespace sftm {
 
 namespace loss {
 
+#ifndef SFTM_DBG_MODE
+#define SFTM_DBG_MODE 0
+#endif
+
 constexpr int kFW = 12;                     // forward warps (3 per SM sub-partition)
 constexpr int kBW = 12;                     // backward warps (3 per SM sub-partition)
 constexpr int kFT = kFW * 32;               // 384 forward threads
@@ -228,7 +232,11 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // the producer with element loads instead, so nothing past the tensor is read.
 template <typename T, int C, bool XP = false, bool UA = false>
 __global__ void __launch_bounds__(kThreads, 1)
-    loss_tmem_kernel(const RowArgs a, int64_t slice_elems, int dbg_mode) {
+    loss_tmem_kernel(const RowArgs a, int64_t slice_elems) {
+  // pipeline-ceiling experiments only (build with EXTRA=-DSFTM_DBG_MODE=n): 1 = no
+  // forward math, 2 = backward stores the raw words, 4 = ... and no dlogits
+  // stores, 8 = no TMEM traffic. Compile-time, so the product build carries none of it.
+  constexpr int dbg_mode = SFTM_DBG_MODE;
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
   static_assert(!UA || (C == 1 && !XP), "unaligned rows run one CTA per row");
   using G = Geo<T>;
@@ -1263,11 +1271,7 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (C > 1) ? 1 : 0;
-  static const int dbg_mode = [] {
-    const char* v = getenv("SFTM_DBG_NOCOMPUTE");  // debug: 1 = no forward math, 2 = no backward math
-    return v ? atoi(v) : 0;
-  }();
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ad, slice, dbg_mode);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ad, slice);
   if (info) {
     info->kernel = XP ? 4 : 2;
     info->cluster = C;
