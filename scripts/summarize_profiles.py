@@ -80,10 +80,14 @@ def full(tag):
     return "\n".join(md)
 
 
-EXTRA = [  # (capture name in gpurun_out, what, command)
-    ("r1_fwd_stream", "forward-only streaming kernel (a1), 131,072 x 151,936 bf16",
+EXTRA = [  # (capture name in gpurun_out or profiles, what, command)
+    ("r2_narrow18992", "fused loss on 18,992-wide rows (a P = 8 vocab shard), 16,384 rows bf16",
+     "scripts/ncu_narrow.sh (python scripts/narrow_rows.py 16384 18992)"),
+    ("r2_wide151936", "fused loss on Qwen3 rows, 16,384 x 151,936 bf16 (isolated launch)",
+     "scripts/ncu_narrow.sh (python scripts/narrow_rows.py 16384 151936)"),
+    ("r1_fwd_stream", "forward-only streaming kernel (a1), 131,072 x 151,936 bf16 (round 1)",
      "scripts/ncu_kernel.sh r1_fwd_stream fwd_stream_kernel 3 python scripts/fwd_only.py"),
-    ("r1_r3_fwd", "R3 gate forward, 48 x 131,072 rows x 128 experts fp32, top-8",
+    ("r1_r3_fwd", "R3 gate forward, 48 x 131,072 rows x 128 experts fp32, top-8 (round 1)",
      "scripts/ncu_kernel.sh r1_r3_fwd r3_fwd_fast 3 python scripts/r3_split.py"),
 ]
 
