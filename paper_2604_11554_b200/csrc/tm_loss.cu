@@ -418,22 +418,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
-    // per-row inputs are loaded one row ahead so their latency never sits on the row boundary
-    float wn = 0.f;
-    int32_t yn = 0;
-    if (cid < a.T) {
-      wn = __ldg(a.w_tok + cid);
-      yn = __ldg(a.targets + cid);
-    }
+    // the row weight is loaded one row ahead so its latency never sits on the row boundary
+    float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
     for (int64_t t = cid; t < a.T; t += ncl) {
       const float wcur = wn;
-      const int32_t ycur = yn;
-      if (t + ncl < a.T) {
-        wn = __ldg(a.w_tok + t + ncl);
-        yn = __ldg(a.targets + t + ncl);
-      }
+      if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
       if (wcur == 0.f) continue;
-      (void)ycur;
       const int mis = row_mis(t);
       const int span = slice_len + mis;  // row extent in sector coordinates
       const int nck_r = UA ? (span + CE - 1) / CE : nck;
@@ -1049,7 +1039,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k == ck) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
-              if (j == jt) gr[j] += gts;
+              gr[j] += (j == jt) ? gts : 0.f;  // select, not an indexed store (keeps gr in registers)
           }
           if (UA && partial) {
 #pragma unroll
@@ -1096,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k == ck) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
-              if (j == jt) gr[j] += gt;
+              gr[j] += (j == jt) ? gt : 0.f;
           }
         } else {
           // entropy term: -p_v (c0 + c1 a_v); the clamp keeps a -inf logit at 0 (not NaN)
@@ -1119,7 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k == ck) {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
-              if (j == jt) gr[j] += gt;
+              gr[j] += (j == jt) ? gt : 0.f;
           }
         }
       general_store:
