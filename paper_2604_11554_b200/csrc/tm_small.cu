@@ -156,9 +156,95 @@ __global__ void grpo_adv_kernel(const float* __restrict__ r, const int32_t* __re
   }
 }
 
+// O(B log B) form for B <= kSortB (one CTA): bitonic sort of (group id, sample)
+// keys in shared memory, then one thread per run of equal ids computes the
+// group's n / mean / min / max / sum of squares in sample-index order (fixed
+// order: deterministic) and writes every member's advantage. The O(B^2) kernel
+// above (one warp per sample scanning all ids) stays for larger B.
+constexpr int kSortB = 16384;
+constexpr int kSortT = 1024;
+
+__global__ void __launch_bounds__(kSortT)
+    grpo_adv_sorted_kernel(const float* __restrict__ r, const int32_t* __restrict__ gid, int B, int n2, float eps,
+                           int std_mode, float* __restrict__ out, int32_t* __restrict__ gsize) {
+  extern __shared__ unsigned long long keys[];  // n2 (power of two >= B) sort keys
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    keys[i] = i < B ? ((static_cast<unsigned long long>(static_cast<uint32_t>(gid[i]) ^ 0x80000000u) << 32) |
+                       static_cast<uint32_t>(i))
+                    : ~0ull;  // padding sorts last
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = keys[i], b = keys[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // runs of equal group ids; within a run the sample indices ascend
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    const uint32_t g = static_cast<uint32_t>(keys[i] >> 32);
+    if (i > 0 && static_cast<uint32_t>(keys[i - 1] >> 32) == g) continue;  // not a run head
+    int e = i + 1;
+    while (e < B && static_cast<uint32_t>(keys[e] >> 32) == g) ++e;
+    const int n = e - i;
+    double sum = 0.0;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int q = i; q < e; ++q) {
+      const float v = r[static_cast<uint32_t>(keys[q])];
+      sum += static_cast<double>(v);
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    const double mean = sum / static_cast<double>(n);
+    double ss = 0.0;
+    if (std_mode != 2)
+      for (int q = i; q < e; ++q) {
+        const double d = static_cast<double>(r[static_cast<uint32_t>(keys[q])]) - mean;
+        ss += d * d;
+      }
+    double den = 1.0;
+    if (std_mode != 2) {
+      const double var = (std_mode == 0) ? ss / static_cast<double>(n - 1) : ss / static_cast<double>(n);
+      den = sqrt(var) + static_cast<double>(eps);
+    }
+    for (int q = i; q < e; ++q) {
+      const uint32_t s_ = static_cast<uint32_t>(keys[q]);
+      double A = 0.0;  // P3: zero-variance group (includes singletons) -> exactly 0
+      if (mx != mn) A = (static_cast<double>(r[s_]) - mean) / den;
+      out[s_] = static_cast<float>(A);
+      if (gsize) gsize[s_] = n;
+    }
+  }
+}
+
 int launch_grpo_advantage(const float* rewards, const int32_t* group_ids, int64_t B, float eps,
                           int std_mode, float* out_adv, int32_t* out_group_size, cudaStream_t s,
                           int* launches) {
+  if (B <= kSortB) {
+    int n2 = 1;
+    while (n2 < B) n2 <<= 1;
+    const size_t smem = sizeof(unsigned long long) * static_cast<size_t>(n2);
+    static PerDevice opted;
+    if (opted() < 0) {
+      cudaFuncSetAttribute(grpo_adv_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(unsigned long long) * kSortB));
+      opted() = 1;
+    }
+    grpo_adv_sorted_kernel<<<1, kSortT, smem, s>>>(rewards, group_ids, static_cast<int>(B), n2, eps, std_mode,
+                                                   out_adv, out_group_size);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const int threads = 256;
   int64_t grid = (B + 7) / 8;
   if (grid > 4096) grid = 4096;

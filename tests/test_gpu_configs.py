@@ -368,3 +368,20 @@ def test_kernels_write_nothing_outside_their_outputs(tm, orc):
     rb, r = guarded(L * T * k, torch.uint8, 201)
     tm.r3_record_layer_major(rec.permute(1, 0, 2).contiguous(), out=r.view(L, T, k))
     check(rb, 201, "record transpose")
+
+
+@pytest.mark.parametrize("B,G", [(1, 1), (7, 3), (4096, 16), (16384, 8), (16385, 5), (20000, 16)])
+def test_grpo_advantage_sizes(tm, orc, B, G):
+    """The sorted single-CTA GRPO kernel (B <= 16,384) and the per-sample scan
+    kernel beyond it: group sizes bit-exact, advantages vs the fp64 oracle,
+    zero-variance groups exactly 0, groups in arbitrary (readiness) order."""
+    rng = np.random.default_rng(B)
+    gids = rng.permutation(np.arange(B) // G).astype(np.int32) * 7 - 3  # non-contiguous, negative ids too
+    r = (rng.random(B) < 0.5).astype(np.float32)
+    r[: min(B, 40)] = 1.0  # some all-equal groups
+    adv, gs = tm.grpo_advantage(f32(r), i32(gids), 1e-6, 0, want_group_size=True)
+    oadv, ogs = orc.grpo_advantage(r, gids)
+    assert np.array_equal(gs.cpu().numpy(), ogs)
+    got = adv.cpu().numpy()
+    assert_close(got, oadv, atol=1e-6, rtol=1e-6, what="advantage")
+    assert np.all(got[oadv == 0.0] == 0.0)
