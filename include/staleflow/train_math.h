@@ -130,6 +130,11 @@ uint64_t sf_tm_launch_count(sf_tm_t h);
  * 5 = the forward-only streaming kernel; *cluster = CTAs
  * per row; *grid = CTAs launched. Any pointer may be NULL. */
 int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* grid);
+/* Row streams of the last fused-loss launch (kernel 2 or 4): 1, 2 or 4 rows of
+ * a CTA in flight side by side, chosen from the row slice width (narrow
+ * vocab-parallel shards run 2 or 4; the environment variable SFTM_LOSS_NS
+ * forces a count for tuning). 1 for every other kernel. */
+int sf_tm_last_launch_streams(sf_tm_t h, int32_t* streams);
 
 /* ---- a6: varlen packing metadata --------------------------------------
  * seq_lens[B] (>= 0), prompt_lens[B] (optional; tokens [0, prompt_len) of a

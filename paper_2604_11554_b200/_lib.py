@@ -73,6 +73,7 @@ _SIGS = {
     "sf_tm_last_error": (ctypes.c_char_p, [_H]),
     "sf_tm_launch_count": (_u64, [_H]),
     "sf_tm_last_launch": (_i32, [_H, _vp, _vp, _vp]),
+    "sf_tm_last_launch_streams": (_i32, [_H, _vp]),
     "sf_tm_varlen_meta": (ctypes.c_int, [_H, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "sf_tm_grpo_advantage": (ctypes.c_int, [_H, _vp, _vp, _i64, _f32, _i32, _vp, _vp, _vp]),
     "sf_tm_logprob_fwd": (ctypes.c_int, [_H, _vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _vp]),

@@ -401,6 +401,12 @@ int sf_tm_last_launch(sf_tm_t h, int32_t* kernel, int32_t* cluster, int32_t* gri
   return SF_TM_OK;
 }
 
+int sf_tm_last_launch_streams(sf_tm_t h, int32_t* streams) {
+  if (!h || !streams) return SF_TM_CONFIG_ERROR;
+  *streams = h->last.streams;
+  return SF_TM_OK;
+}
+
 int sf_tm_varlen_meta(sf_tm_t h, const int32_t* seq_lens, const int32_t* prompt_lens,
                       const int32_t* group_ids, int64_t B, int64_t T, int32_t* cu_seqlens,
                       int32_t* seq_id, uint8_t* mask, int32_t* tok_group, void* stream) {

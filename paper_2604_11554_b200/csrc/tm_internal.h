@@ -97,6 +97,7 @@ struct LaunchInfo {
   int cluster = 1;
   int grid = 0;
   int launches = 0;
+  int streams = 1;  // row streams of the fused loss kernel (1 = one row at a time per CTA)
 };
 
 // Launches the row kernel for `mode`. Returns 0 or a cudaError_t value; on a

@@ -230,7 +230,47 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // the boundary dlogits vectors are stored per element. Reads extend to whole
 // 16-B sectors inside the tensor; the very last row's tail sector is filled by
 // the producer with element loads instead, so nothing past the tensor is read.
-template <typename T, int C, bool XP = false, bool UA = false>
+// NS (C == 1, aligned rows): row streams. The 12 forward / backward warp pairs
+// split into NS groups of 12/NS pairs; consecutive loss-active rows of the CTA
+// go to the streams in turn, and every ring / row-store slot carries one
+// 12/NS-KB sub-chunk of each stream's row (the producer fills it with NS bulk
+// copies). A warp then handles only every NS-th row, so the per-row work of
+// the compute warps (row-end merge, chunk-0 base, tail chunk, scalar
+// hand-off) is spent 1/NS as often per SM — what bounds narrow rows (a
+// vocab-parallel shard at P = 4 / 8). Streams advance in lockstep: the NS rows
+// of a group have the same width, and a stream with no row in the CTA's last
+// group idles through its steps.
+#ifdef SFTM_HANG_DEBUG
+// Debug build only (EXTRA=-DSFTM_HANG_DEBUG, scripts/hang_debug.py): a wait that
+// gives up after 2 s and records where, so a protocol deadlock shows its
+// waiting sites instead of hanging the GPU. dbg[0]: the first give-up (line |
+// parity << 16 | barrier offset << 20 | CTA << 40 | warp << 56); dbg[16 + 32 *
+// CTA + warp]: each warp's first give-up; dbg[15]: abort flag (later waits give
+// up at once).
+__device__ __forceinline__ void kwait(unsigned long long* dbg, int line, uint32_t bar, uint32_t par) {
+  if (mbar_try_wait(bar, par)) return;
+  volatile unsigned long long* vd = dbg;  // host-mapped (pinned) memory: readable after a fault
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait(bar, par)) {
+    if (vd[15] != 0ull || globaltimer_ns() - t0 > 2000000000ull) {
+      const unsigned long long rec = static_cast<unsigned long long>(line) | (static_cast<unsigned long long>(par) << 16) |
+                                     (static_cast<unsigned long long>(bar & 0xffffu) << 20) |
+                                     (static_cast<unsigned long long>(blockIdx.x) << 40) |
+                                     (static_cast<unsigned long long>(threadIdx.x >> 5) << 56);
+      if (vd[16 + blockIdx.x * 32 + (threadIdx.x >> 5)] == 0ull) vd[16 + blockIdx.x * 32 + (threadIdx.x >> 5)] = rec;
+      if (vd[15] == 0ull) vd[0] = rec;
+      vd[15] = 1ull;
+      __threadfence_system();
+      return;
+    }
+  }
+}
+#define KWAIT(bar, par) kwait(a.dbg, __LINE__, bar, par)
+#else
+#define KWAIT(bar, par) mbar_wait(bar, par)
+#endif
+
+template <typename T, int C, bool XP = false, bool UA = false, int NS = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     loss_tmem_kernel(const RowArgs a, int64_t slice_elems) {
   // pipeline-ceiling experiments only (build with EXTRA=-DSFTM_DBG_MODE=n): 1 = no
@@ -239,10 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int dbg_mode = SFTM_DBG_MODE;
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
   static_assert(!UA || (C == 1 && !XP), "unaligned rows run one CTA per row");
+  static_assert(NS == 1 || (C == 1 && !UA), "row streams: one CTA per row slice, aligned rows");
+  static_assert(NS == 1 || NS == 2 || NS == 4, "row streams");
   using G = Geo<T>;
   constexpr int CE = G::CE;
   constexpr int NE = G::NE;
   constexpr int EV = G::EV;
+  constexpr int SW = kFW / NS;       // warp pairs per row stream
+  constexpr int SCE = CE / NS;       // elements of one stream's sub-chunk of a slot
+  constexpr int SCB = kCB / NS;      // ... and its bytes
+  constexpr int SHALF = SCE / 2;     // a thread's second vector starts here (sub-chunk coordinates)
+  constexpr int RD = (2 * NS > kRD) ? 2 * NS : kRD;  // per-row rings hold two groups of rows
 
   extern __shared__ __align__(1024) uint8_t ring[];
   __shared__ __align__(8) uint64_t full_bar[kSlots];
@@ -251,10 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t tempty_bar[kStore];
   __shared__ __align__(8) uint64_t mail_bar[kMailD];
   __shared__ __align__(16) float4 mail[kMailD][8];
-  __shared__ __align__(16) float4 red[kRD][kFW];      // per forward warp: (m2, s, w, z_target|NaN)
-  __shared__ __align__(8) uint64_t red_bar[kRD], red_free[kRD];
-  __shared__ __align__(16) RowScal scal[kRD];
-  __shared__ __align__(8) uint64_t scal_bar[kRD], scal_free[kRD];
+  __shared__ __align__(16) float4 red[RD][SW];       // per forward warp of the row's stream: (m2, s, w, -)
+  __shared__ __align__(8) uint64_t red_bar[RD], red_free[RD];
+  __shared__ __align__(16) RowScal scal[RD];
+  __shared__ __align__(8) uint64_t scal_bar[RD], scal_free[RD];
   __shared__ __align__(8) uint64_t rcv_done[kCredD];  // XP: receiver progress (sender credit)
   __shared__ uint32_t tmem_base_sh;
   __shared__ uint32_t sink_sh[kBW];
@@ -270,8 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (sl64 > slice_elems) sl64 = slice_elems;
   if (sl64 < 0) sl64 = 0;
   const int slice_len = static_cast<int>(sl64);
-  const int nck = (slice_len + CE - 1) / CE;
-  const int nfull = slice_len / CE;
+  const int nck = (slice_len + SCE - 1) / SCE;
+  const int nfull = slice_len / SCE;
   const uint32_t ring_base = smem_u32(ring);
   const uint32_t stash_base = ring_base + kSlots * kCB;  // smem row-store slot i = store slot kTSlots + i
 
@@ -285,11 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&tempty_bar[i]), kFT);  // backward threads (same count)
     }
     for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
-    for (int i = 0; i < kRD; ++i) {
-      mbar_init(smem_u32(&red_bar[i]), kFW);  // lane 0 of each forward warp
+    for (int i = 0; i < RD; ++i) {
+      mbar_init(smem_u32(&red_bar[i]), SW);   // lane 0 of each forward warp of the row's stream
       mbar_init(smem_u32(&red_free[i]), 1);   // lane 0 of the control warp that read it
       mbar_init(smem_u32(&scal_bar[i]), 1);   // lane 0 of the control warp that wrote it
-      mbar_init(smem_u32(&scal_free[i]), kBW);  // lane 0 of each backward warp
+      mbar_init(smem_u32(&scal_free[i]), SW);  // lane 0 of each backward warp of the row's stream
     }
     for (int i = 0; i < kCredD; ++i) mbar_init(smem_u32(&rcv_done[i]), 1);
     fence_mbar_init();
@@ -328,9 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // backward partner (same element mapping) take the same decision.
   auto warp_idle = [&](int k, bool partial, int mis, int span, int wbase) -> bool {
     if (!partial) return false;
-    const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+    const int rem = span - k * SCE, lo = (UA && k == 0) ? mis : 0;
     const int a0 = EV * wbase, a1 = EV * (wbase + 32);  // the warp's first-vector block
-    const int b0 = G::HALF + a0, b1 = G::HALF + a1;     // ... and second-vector block
+    const int b0 = SHALF + a0, b1 = SHALF + a1;         // ... and second-vector block
     return !(a0 < rem && a1 > lo) && !(b0 < rem && b1 > lo);
   };
   // where the backward finds the target column (computed once per row by the
@@ -340,17 +387,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     town = 0;
     if (yl64 >= 0 && yl64 < slice_len) {
       const int yp = static_cast<int>(yl64) + mis;  // sector coordinates
-      const int r = yp % CE;
-      const int v = r >= G::HALF ? 1 : 0;
-      const int rr = r - v * G::HALF;
-      tck = yp / CE;
+      const int r = yp % SCE;
+      const int v = r >= SHALF ? 1 : 0;
+      const int rr = r - v * SHALF;
+      tck = yp / SCE;
       town = (static_cast<uint32_t>(rr / EV) << 8) | static_cast<uint32_t>(v * EV + rr % EV);
     }
   };
 
   if (warp == kProd) {
     // ================================================================ producer
-    if (lane == 0) {
+    if (NS > 1 && lane == 0) {
+      // row streams: a group of up to NS loss-active rows, one per stream;
+      // slot step k carries sub-chunk k of every row of the group
+      const uint64_t pol = l2_evict_first_policy();
+      uint32_t slot = 0, ph = 0;
+      int64_t grow[NS];
+      int ng = 0;
+      auto issue_group = [&]() {
+        for (int k = 0; k < nck; ++k) {
+          const int rem = slice_len - k * SCE;
+          const uint32_t bytes = static_cast<uint32_t>(rem < SCE ? rem : SCE) * G::es;
+          DBG_WAIT(w_a, KWAIT(smem_u32(&empty_bar[slot]), ph ^ 1u));
+          mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes * static_cast<uint32_t>(ng));
+#pragma unroll
+          for (int g = 0; g < NS; ++g)
+            if (g < ng)
+              bulk_g2s(ring_base + slot * kCB + g * SCB, logits + grow[g] * a.ld + static_cast<int64_t>(k) * SCE,
+                       bytes, smem_u32(&full_bar[slot]), pol);
+          if (++slot == kSlots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      };
+      float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
+      for (int64_t t = cid; t < a.T; t += ncl) {
+        const float wcur = wn;
+        if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
+        if (wcur == 0.f) continue;
+#pragma unroll
+        for (int g = 0; g < NS; ++g)
+          if (g == ng) grow[g] = t;  // register-resident (no dynamic index)
+        if (++ng == NS) {
+          issue_group();
+          ng = 0;
+        }
+      }
+      if (ng > 0) issue_group();
+    } else if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       uint32_t slot = 0, ph = 0;
       float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;  // next row's weight, one row ahead
@@ -363,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nck_r = UA ? (span + CE - 1) / CE : nck;
         const T* row = logits + t * a.ld + slice_start - mis;
         for (int k = 0; k < nck_r; ++k) {
-          const int rem = span - k * CE;
+          const int rem = span - k * SCE;
           uint32_t bytes = static_cast<uint32_t>(rem < CE ? rem : CE) * G::es;
           int tail = 0;  // UA: elements of a final partial sector loaded by this lane
           if constexpr (UA) {
@@ -374,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               bytes = (bytes + 15u) & ~15u;  // whole sectors (inside the tensor)
             }
           }
-          DBG_WAIT(w_a, mbar_wait(smem_u32(&empty_bar[slot]), ph ^ 1u));
+          DBG_WAIT(w_a, KWAIT(smem_u32(&empty_bar[slot]), ph ^ 1u));
           if constexpr (UA) {
             const T* tp = row + static_cast<int64_t>(k) * CE + bytes / G::es;
             uint8_t* ts_ = ring + slot * kCB + bytes;
@@ -399,12 +484,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // critical path (its row statistics gate the backward).
     const int fw = warp - kBW;                 // 0..kFW-1
     const int ftid = tid - kBW * 32;           // 0..kFT-1
+    const int sg = fw / SW;                    // row stream
+    const int sid = ftid - sg * (SW * 32);     // thread index within the stream
     const uint32_t tlane = static_cast<uint32_t>(32 * (fw & 3)) << 16;
     const uint32_t tcol = 8u * static_cast<uint32_t>(fw >> 2);  // 8 columns per warp of a sub-partition
     const float c = a.inv_tau * kLog2e;
     const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
     const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
-    const uint32_t ring_t = ring_base + 16u * ftid;
+    const uint32_t ring_t = ring_base + static_cast<uint32_t>(sg * SCB) + 16u * sid;
     const uint32_t stash_t = stash_base + 16u * ftid;
     const uint32_t tm_t = tbase + tlane + tcol;
     // row-store read-back (repair path)
@@ -418,12 +505,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     uint32_t slot = 0, ph = 0, ts = 0, tph = 0, nrow = 0;
+    // a thread's j-th element within its stream's sub-chunk
+    auto eoff = [&](int j) { return (j < EV) ? (EV * sid + j) : (SHALF + EV * sid + (j - EV)); };
+    // one slot step with nothing of this warp in it: keep the barrier protocol
+    auto fidle = [&]() {
+      DBG_WAIT(w_a, KWAIT(full0 + 8u * slot, ph));
+      mbar_arrive(empty0 + 8u * slot);  // nothing read from the slot
+      if (++slot == kSlots) {
+        slot = 0;
+        ph ^= 1u;
+      }
+      DBG_WAIT(w_b, KWAIT(tempty0 + 8u * ts, tph ^ 1u));
+      mbar_arrive(tfull0 + 8u * ts);  // nothing written to the row-store slot
+      if (++ts == kStore) {
+        ts = 0;
+        tph ^= 1u;
+      }
+    };
     // the row weight is loaded one row ahead so its latency never sits on the row boundary
     float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
     for (int64_t t = cid; t < a.T; t += ncl) {
       const float wcur = wn;
       if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
       if (wcur == 0.f) continue;
+      if (NS > 1 && static_cast<int>(nrow % NS) != sg) {  // another stream's row
+        ++nrow;
+        continue;
+      }
       const int mis = row_mis(t);
       const int span = slice_len + mis;  // row extent in sector coordinates
       const int nck_r = UA ? (span + CE - 1) / CE : nck;
@@ -437,27 +545,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // chunk 0; `partial` masks elements past the slice end. Both are constants
       // at every call site, so the hot loop carries no per-chunk branches.
       auto chunk = [&](int k, bool first, bool partial) {
-        if (warp_idle(k, partial, mis, span, 32 * fw)) {
-          DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
-          mbar_arrive(empty0 + 8u * slot);  // nothing read from the slot
-          if (++slot == kSlots) {
-            slot = 0;
-            ph ^= 1u;
-          }
-          DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
+        if (warp_idle(k, partial, mis, span, 32 * (fw % SW))) {
           if (first) m2 = 0.f;  // no element of this warp in the row's only chunk
-          mbar_arrive(tfull0 + 8u * ts);  // nothing written to the row-store slot
-          if (++ts == kStore) {
-            ts = 0;
-            tph ^= 1u;
-          }
+          fidle();
           return;
         }
-        DBG_WAIT(w_a, mbar_wait(full0 + 8u * slot, ph));
+        DBG_WAIT(w_a, KWAIT(full0 + 8u * slot, ph));
         const uint32_t sa = ring_t + slot * kCB;
         uint4 v0 = lds128(sa);
-        uint4 v1 = lds128(sa + kCB / 2);
-        DBG_WAIT(w_b, mbar_wait(tempty0 + 8u * ts, tph ^ 1u));
+        uint4 v1 = lds128(sa + SCB / 2);
+        DBG_WAIT(w_b, KWAIT(tempty0 + 8u * ts, tph ^ 1u));
         const bool in_tmem = ts < kTSlots;
         if (in_tmem) {
           tc_fence_after();
@@ -478,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float x[NE];
         unpack(logits, v0, v1, x);
-        const int rem = span - k * CE;             // valid elements end here (chunk coordinates)
+        const int rem = span - k * SCE;             // valid elements end here (chunk coordinates)
         const int lo = (UA && k == 0) ? mis : 0;   // ... and start here
         if (first) {
           // Later elements may exceed this base (arguments > 0 are fine); only a
@@ -486,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float xm = -INFINITY;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
-            const int pj = elem_off<T>(ftid, j);
+            const int pj = eoff(j);
             if (!partial || (pj >= lo && pj < rem)) xm = fmaxf(xm, x[j]);
           }
           m2 = xm * c;
@@ -510,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int p0 = v * G::HALF + EV * ftid;
+            const int p0 = v * SHALF + EV * sid;
             if (p0 >= lo && p0 + EV <= rem) {
 #pragma unroll
               for (int q = 0; q < EV / 2; ++q) {
@@ -538,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // vector, so each of this thread's two vectors lies wholly inside or
           // outside the slice: the packed path, per vector.
           // A -inf logit makes w NaN here as on full chunks -> row-end repair.
-          const bool ok0 = EV * ftid < rem, ok1 = G::HALF + EV * ftid < rem;
+          const bool ok0 = EV * sid < rem, ok1 = SHALF + EV * sid < rem;
           const float2 c2 = make_float2(c, c), nm2 = make_float2(-m2, -m2);
 #pragma unroll
           for (int p = 0; p < NE / 2; ++p) {
@@ -594,10 +691,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
-          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+          const int rem = span - k * SCE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
-            const int pj = elem_off<T>(ftid, j);
+            const int pj = eoff(j);
             if (pj >= lo && pj < rem) mx = fmaxf(mx, x[j]);
           }
           if (++q == kStore) q = 0;
@@ -610,10 +707,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           load_store(q, v0r, v1r);
           float x[NE];
           unpack(logits, v0r, v1r, x);
-          const int rem = span - k * CE, lo = (UA && k == 0) ? mis : 0;
+          const int rem = span - k * SCE, lo = (UA && k == 0) ? mis : 0;
 #pragma unroll
           for (int j = 0; j < NE; ++j) {
-            const int pj = elem_off<T>(ftid, j);
+            const int pj = eoff(j);
             if (pj >= lo && pj < rem && x[j] != -INFINITY) {
               const float av = fmaf(x[j], c, -mb2);
               const float e = ex2(av);
@@ -630,14 +727,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // merges the 12 partials, so forward warps go straight to the next row.
       my = warp_merge(my);
       if (lane == 0) {
-#ifndef SFTM_NO_FLOWCTL  // A/B timing only: unsafe when the forward runs > kRD rows ahead
-        mbar_wait(smem_u32(&red_free[nrow % kRD]), ((nrow / kRD) & 1u) ^ 1u);
-#endif
-        red[nrow % kRD][fw] = make_float4(my.m2, my.s, my.w, 0.f);
-        mbar_arrive(smem_u32(&red_bar[nrow % kRD]));
+        KWAIT(smem_u32(&red_free[nrow % RD]), ((nrow / RD) & 1u) ^ 1u);
+        red[nrow % RD][fw % SW] = make_float4(my.m2, my.s, my.w, 0.f);
+        mbar_arrive(smem_u32(&red_bar[nrow % RD]));
       }
       ++nrow;
     }
+    // the CTA's last group of rows has no row for this stream: idle through its steps
+    if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS))
+      for (int k = 0; k < nck; ++k) fidle();
   } else if (warp >= kCtl) {
     // ================================================================ control
     // Per row: merge the 12 forward partials, exchange with the cluster through
@@ -696,16 +794,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
         if (ci == 0) {
           // ------------------------------------------------ sender
-          const uint32_t rs = nrow % kRD;
+          const uint32_t rs = nrow % RD;
           float zy = __int_as_float(0x7fc00000);
           if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
           if (nrow >= static_cast<uint32_t>(kXpCredit)) {
             const uint32_t m = nrow - kXpCredit;
-            mbar_wait(smem_u32(&rcv_done[m % kCredD]), (m / kCredD) & 1u);
+            KWAIT(smem_u32(&rcv_done[m % kCredD]), (m / kCredD) & 1u);
           }
-          DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), (nrow / kRD) & 1u));
+          DBG_WAIT(w_a, KWAIT(smem_u32(&red_bar[rs]), (nrow / RD) & 1u));
           Stats v = stats_empty();
-          if (lane < kFW) {
+          if (lane < SW) {
             const float4 r = red[rs][lane];
             v = Stats{r.x, r.y, r.z};
           }
@@ -718,8 +816,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else if (static_cast<int>(nrow % (kNCtl - 1)) == ci - 1) {
           // ------------------------------------------------ receivers (rows alternate)
-          const uint32_t rs = nrow % kRD;
-          const uint32_t rpar = (nrow / kRD) & 1u;
+          const uint32_t rs = nrow % RD;
+          const uint32_t rpar = (nrow / RD) & 1u;
           const int64_t yl64 = yg - slice_start;
           float4 mv = make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fc00000));
           if (lane < a.xp_P) {
@@ -781,7 +879,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             r.lse2f = lse2 - log2f(fabsf(r.c0));
             r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
             target_slot(yl64, row_mis(t), r.tck, r.town);
-            mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
+            if (NS > 1 && nrow > 0) {  // publish in row order (see the plain control path)
+              const uint32_t p = nrow - 1;
+              KWAIT(smem_u32(&scal_bar[p % RD]), (p / RD) & 1u);
+            }
+            KWAIT(smem_u32(&scal_free[rs]), rpar ^ 1u);
             scal[rs] = r;
             mbar_arrive(smem_u32(&scal_bar[rs]));
             mbar_arrive(smem_u32(&rcv_done[nrow % kCredD]));  // the shuffles consumed the messages
@@ -822,31 +924,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++nrow;
         continue;
       }
-      const uint32_t rs = nrow % kRD;
-      const uint32_t rpar = (nrow / kRD) & 1u;
+      const uint32_t rs = nrow % RD;
+      const uint32_t rpar = (nrow / RD) & 1u;
       const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
       const int64_t yl64 = yg - slice_start;
-      // z_target straight from HBM, issued before the partials wait; the release
-      // arrive of the exchange below orders this read before any dlogits write
-      // of the row (in-place dlogits stays safe)
+      // z_target straight from HBM, issued before the partials wait; the
+      // published scalars depend on it, so the read completes before their
+      // release arrive and thus before any dlogits write of the row (in-place
+      // dlogits stays safe)
       float zy = __int_as_float(0x7fc00000);
       if (yg >= 0 && yg < a.V) zy = ldg_elem(logits, t * a.ld + yg) * a.inv_tau;
-      DBG_WAIT(w_a, mbar_wait(smem_u32(&red_bar[rs]), rpar));
+      if (NS > 1 && nrow > 0) {
+        // Row streams finish the rows of a group out of order, so a control
+        // warp could reach this slot's wait before row nrow - RD was even
+        // written and take that phase for its own (parity aliasing). Consuming
+        // the partials strictly in row order (row nrow - 1 first) rules it out.
+        const uint32_t p = nrow - 1;
+        KWAIT(smem_u32(&red_free[p % RD]), (p / RD) & 1u);
+      }
+      DBG_WAIT(w_a, KWAIT(smem_u32(&red_bar[rs]), rpar));
       Stats v = stats_empty();
-      if (lane < kFW) {
+      if (lane < SW) {
         const float4 r = red[rs][lane];
         v = Stats{r.x, r.y, r.z};
       }
       v = warp_merge(v);
       if (lane == 0) mbar_arrive(smem_u32(&red_free[rs]));  // the shuffles consumed every lane's read
-      const float z = 0.f;
-      const uint32_t mb = nrow % kMailD;
       Stats st = stats_empty();
-      if (lane == 0) {
-        if (C == 1) {
-          mail[mb][0] = make_float4(v.m2, v.s, v.w, z);
-          mbar_arrive(smem_u32(&mail_bar[mb]));
-        } else {
+      if constexpr (C == 1) {
+        st = stats_merge(st, v);  // one CTA per row: no exchange
+      } else {
+        const float z = 0.f;
+        const uint32_t mb = nrow % kMailD;
+        if (lane == 0) {
           const uint32_t my_slot = smem_u32(&mail[mb][crank]);
           const uint32_t my_bar = smem_u32(&mail_bar[mb]);
 #pragma unroll
@@ -855,16 +965,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_remote(mapa(my_bar, q));
           }
         }
-      }
-      if (C == 1) {
-        DBG_WAIT(w_b, mbar_wait(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u));
-      } else {
         DBG_WAIT(w_b, mbar_wait_cluster_lite(smem_u32(&mail_bar[mb]), (nrow / kMailD) & 1u));
-      }
 #pragma unroll
-      for (int q = 0; q < C; ++q) {
-        const float4 mv = mail[mb][q];
-        st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
+        for (int q = 0; q < C; ++q) {
+          const float4 mv = mail[mb][q];
+          st = stats_merge(st, Stats{mv.x, mv.y, mv.z});
+        }
       }
       float lse2, lse, H, logp;
       row_scalars(st, zy, lse2, lse, H, logp);
@@ -887,9 +993,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         r.lse2f = lse2 - log2f(fabsf(r.c0));
         r.sgn = r.c0 > 0.f ? 0x80008000u : 0u;
         target_slot(yl64, row_mis(t), r.tck, r.town);
-#ifndef SFTM_NO_FLOWCTL
-        mbar_wait(smem_u32(&scal_free[rs]), rpar ^ 1u);
-#endif
+        if (NS > 1 && nrow > 0) {
+          // publish in row order (row nrow - 1 first): then row nrow - RD was
+          // published, its backward waited, and this slot's free phase below
+          // cannot alias an older one
+          const uint32_t p = nrow - 1;
+          KWAIT(smem_u32(&scal_bar[p % RD]), (p / RD) & 1u);
+        }
+        KWAIT(smem_u32(&scal_free[rs]), rpar ^ 1u);
         scal[rs] = r;
         mbar_arrive(smem_u32(&scal_bar[rs]));
       }
@@ -915,6 +1026,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================================================================ backward
     const int btid = tid;                     // same element mapping as forward warp warp+kBW
     const int bw = warp;
+    const int sg = bw / SW;                   // row stream (as its partner forward warp)
+    const int sid = btid - sg * (SW * 32);    // thread index within the stream
     const uint32_t tlane = static_cast<uint32_t>(32 * (bw & 3)) << 16;
     const uint32_t tcol = 8u * static_cast<uint32_t>(bw >> 2);
     const float c = a.inv_tau * kLog2e;
@@ -948,16 +1061,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
+      if (NS > 1 && static_cast<int>(nrow % NS) != sg) {  // another stream's row
+        ++nrow;
+        continue;
+      }
       const int mis = row_mis(t);
       const int span = slice_len + mis;  // row extent in sector coordinates
       const int nck_r = UA ? (span + CE - 1) / CE : nck;
-      const uint32_t rs = nrow % kRD;
-      const uint32_t rpar = (nrow / kRD) & 1u;
-      DBG_WAIT(w_a, mbar_wait(smem_u32(&scal_bar[rs]), rpar));
+      const uint32_t rs = nrow % RD;
+      const uint32_t rpar = (nrow / RD) & 1u;
+      DBG_WAIT(w_a, KWAIT(smem_u32(&scal_bar[rs]), rpar));
       const RowScal rsc = scal[rs];
       const float lse2 = rsc.lse2, lse2f = rsc.lse2f, c0 = rsc.c0, c1 = rsc.c1, gt = rsc.gt;
       const bool neg = rsc.sgn != 0u;
-      const int ck = (static_cast<int>(rsc.town >> 8) == btid) ? rsc.tck : -1;
+      const int ck = (static_cast<int>(rsc.town >> 8) == sid) ? rsc.tck : -1;
       const int jt = static_cast<int>(rsc.town & 0xffu);
       // dlogits rows share the logits rows' sector phase (checked at dispatch)
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start - mis;
@@ -967,8 +1084,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // into the exponent and the sign applied to the packed words, 1 = no
       // entropy term, 2 = entropy term. `partial` masks past the slice end.
       auto bchunk = [&](int k, bool partial, int mode) {
-        if (warp_idle(k, partial, mis, span, 32 * bw)) {
-          DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
+        if (warp_idle(k, partial, mis, span, 32 * (bw % SW))) {
+          DBG_WAIT(w_b, KWAIT(tfull0 + 8u * ts, tph));
           mbar_arrive(tempty0 + 8u * ts);  // nothing read from the row-store slot
           if (++ts == kStore) {
             ts = 0;
@@ -976,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           return;
         }
-        DBG_WAIT(w_b, mbar_wait(tfull0 + 8u * ts, tph));
+        DBG_WAIT(w_b, KWAIT(tfull0 + 8u * ts, tph));
         tc_fence_after();
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
         // TMEM slots are released once tcgen05.wait::ld returned; smem-store
@@ -999,12 +1116,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           ts = 0;
           tph ^= 1u;
         }
-        T* dst = drow + k * CE;
-        const int rem = span - k * CE;
+        T* dst = drow + k * SCE;
+        const int rem = span - k * SCE;
         if (!partial && (dbg_mode & 2)) {  // debug: store the words back (pipeline ceiling)
           if (!(dbg_mode & 4)) {
-            stg128_cs(dst + EV * btid, w0);
-            stg128_cs(dst + G::HALF + EV * btid, w1);
+            stg128_cs(dst + EV * sid, w0);
+            stg128_cs(dst + SHALF + EV * sid, w1);
           }
           if (late) {
             __threadfence_block();  // debug path: order the LDS before the release
@@ -1020,8 +1137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool vok0 = true, vok1 = true;
         if (partial) {
           const int lo = (UA && k == 0) ? mis : 0;
-          vok0 = (EV * btid + EV > lo) && (EV * btid < rem);
-          vok1 = (G::HALF + EV * btid + EV > lo) && (G::HALF + EV * btid < rem);
+          vok0 = (EV * sid + EV > lo) && (EV * sid < rem);
+          vok1 = (SHALF + EV * sid + EV > lo) && (SHALF + EV * sid < rem);
         }
         const uint32_t dep = w0.x ^ w1.w ^ __float_as_uint(lse2f) ^ rsc.sgn;
         if (mode == 0) {
@@ -1056,13 +1173,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           p1.z = pack_bf16x2(gr[12], gr[13]) ^ sgn;
           p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
           if (!partial) {
-            stg128_cs(dst + EV * btid, p0);
-            stg128_cs(dst + G::HALF + EV * btid, p1);
+            stg128_cs(dst + EV * sid, p0);
+            stg128_cs(dst + SHALF + EV * sid, p1);
           } else {
             // vector-granular tail (see the forward's partial chunk)
-            const bool s0 = EV * btid < rem, s1 = G::HALF + EV * btid < rem;
-            if (s0) stg128_cs(dst + EV * btid, p0);
-            if (s1) stg128_cs(dst + G::HALF + EV * btid, p1);
+            const bool s0 = EV * sid < rem, s1 = SHALF + EV * sid < rem;
+            if (s0) stg128_cs(dst + EV * sid, p0);
+            if (s1) stg128_cs(dst + SHALF + EV * sid, p1);
             // a thread storing nothing still orders its loads before the
             // releases below through a dependent (dummy) smem store
             if (!s0) sink_u32(sink_a, p0.x ^ p1.y ^ dep);
@@ -1114,8 +1231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       general_store:
         if (!partial) {
-          store_vec(dst + EV * btid, gr);
-          store_vec(dst + G::HALF + EV * btid, gr + EV);
+          store_vec(dst + EV * sid, gr);
+          store_vec(dst + SHALF + EV * sid, gr + EV);
         } else if (UA) {
           // front/tail chunk of an unaligned row: whole vectors where they are
           // entirely inside the row, element stores on the boundary vectors
@@ -1123,7 +1240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool any = false;
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int p0 = v * G::HALF + EV * btid;
+            const int p0 = v * SHALF + EV * sid;
             if (p0 >= lo && p0 + EV <= rem) {
               store_vec(dst + p0, gr + v * EV);
               any = true;
@@ -1138,9 +1255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (!any) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
         } else {
-          const bool s0 = EV * btid < rem;
-          if (s0) store_vec(dst + EV * btid, gr);
-          if (G::HALF + EV * btid < rem) store_vec(dst + G::HALF + EV * btid, gr + EV);
+          const bool s0 = EV * sid < rem;
+          if (s0) store_vec(dst + EV * sid, gr);
+          if (SHALF + EV * sid < rem) store_vec(dst + SHALF + EV * sid, gr + EV);
           if (!s0) sink_u32(sink_a, __float_as_uint(gr[0]) ^ __float_as_uint(gr[NE - 1]) ^ dep);
         }
         if (late) mbar_arrive(rel);
@@ -1184,6 +1301,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;
     }
+    // the CTA's last group of rows has no row for this stream: idle through its steps
+    if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS)) {
+      for (int k = 0; k < nck; ++k) {
+        DBG_WAIT(w_b, KWAIT(tfull0 + 8u * ts, tph));
+        mbar_arrive(tempty0 + 8u * ts);  // nothing read from the row-store slot
+        if (++ts == kStore) {
+          ts = 0;
+          tph ^= 1u;
+        }
+      }
+    }
   }
 
   if (dbg && lane == 0) {
@@ -1203,9 +1331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
-template <typename T, int C, bool XP = false, bool UA = false>
+template <typename T, int C, bool XP = false, bool UA = false, int NS = 1>
 int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  auto kern = loss_tmem_kernel<T, C, XP, UA>;
+  auto kern = loss_tmem_kernel<T, C, XP, UA, NS>;
   static PerDevice cache;  // per instantiation and device
   int& max_active = cache();
   {
@@ -1267,8 +1395,36 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
     info->cluster = C;
     info->grid = static_cast<int>(ncl * C);
     info->launches = 1;
+    info->streams = NS;
   }
   return e;
+}
+
+// Row streams for a one-CTA row slice of `slice` elements: the most streams
+// whose per-stream row still leaves the row store room for two rows (so the
+// forward of one group overlaps the backward of the previous one).
+// SFTM_LOSS_NS=1|2|4 forces a count (tuning, tests).
+template <typename T>
+int pick_streams(int64_t slice) {
+  using G = Geo<T>;
+  static const int forced = [] {
+    const char* v = getenv("SFTM_LOSS_NS");
+    return v ? atoi(v) : 0;
+  }();
+  auto fits = [&](int ns, int64_t lim) { return (slice + G::CE / ns - 1) / (G::CE / ns) <= lim; };
+  if ((forced == 1 || forced == 2 || forced == 4) && fits(forced, kMaxChunks)) return forced;
+  for (int ns : {4, 2})
+    if (fits(ns, kStore / 2)) return ns;
+  return 1;
+}
+
+template <typename T, bool XP>
+int launch_streams(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
+  switch (pick_streams<T>(slice)) {
+    case 4: return launch_c<T, 1, XP, false, 4>(a, slice, s, info);
+    case 2: return launch_c<T, 1, XP, false, 2>(a, slice, s, info);
+  }
+  return launch_c<T, 1, XP, false, 1>(a, slice, s, info);
 }
 
 template <typename T>
@@ -1277,7 +1433,7 @@ int launch_with(const RowArgs& a, int C, cudaStream_t s, LaunchInfo* info) {
   int64_t slice = (a.V + C - 1) / C;
   slice = (slice + G::EV - 1) / G::EV * G::EV;  // 16-B aligned slice starts
   switch (C) {
-    case 1: return launch_c<T, 1>(a, slice, s, info);
+    case 1: return launch_streams<T, false>(a, slice, s, info);
     case 2: return launch_c<T, 2>(a, slice, s, info);
     case 3: return launch_c<T, 3>(a, slice, s, info);
     case 4: return launch_c<T, 4>(a, slice, s, info);
@@ -1338,7 +1494,7 @@ int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
     using G = loss::Geo<T>;
     int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
     if ((slice + G::CE - 1) / G::CE > loss::kMaxChunks) return -2;
-    return loss::launch_c<T, 1, true>(a, slice, s, info);
+    return loss::launch_streams<T, true>(a, slice, s, info);
   };
   if (a.dtype == 1) return go(uint16_t{});
   return go(float{});

@@ -63,7 +63,10 @@ class Handle:
                    "sf_tm_last_launch")
         names = {0: "rows_ring_kernel", 1: "rows_generic_kernel", 2: "loss_tmem_kernel",
                  4: "loss_tmem_kernel[peer-exchange]", 5: "fwd_stream_kernel"}
-        return {"kernel": names.get(k.value, str(k.value)), "cluster": c.value, "grid": g.value}
+        ns = ctypes.c_int32()
+        self.check(_lib.lib().sf_tm_last_launch_streams(self._h, ctypes.byref(ns)), "sf_tm_last_launch_streams")
+        return {"kernel": names.get(k.value, str(k.value)), "cluster": c.value, "grid": g.value,
+                "streams": ns.value}
 
     def close(self):
         if self._h:

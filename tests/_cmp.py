@@ -63,7 +63,9 @@ def loss_row_scale(og, w, a, olp, old, ref, beta=0.0, kl_mode=0, ent=0.0, inv_ta
     w = np.abs(np.asarray(w, np.float64))
     ratio = np.exp(np.asarray(olp, np.float64) - np.asarray(old, np.float64))
     d = np.asarray(ref, np.float64) - np.asarray(olp, np.float64)
-    dkl = {0: np.abs(1 - np.exp(np.minimum(d, 80))), 1: np.ones_like(d), 2: np.abs(d), 3: np.ones_like(d)}[kl_mode]
+    # k3's derivative 1 - e^d is a difference of two O(1) terms: an fp32 logp
+    # error eps moves it by ~eps * e^d however small |1 - e^d| is
+    dkl = {0: 1 + np.exp(np.minimum(d, 80)), 1: np.ones_like(d), 2: np.abs(d), 3: np.ones_like(d)}[kl_mode]
     terms = np.abs(np.asarray(a, np.float64)) * ratio + abs(beta) * dkl
     return (np.abs(og) + w * terms + w * abs(ent) * 60.0) * inv_tau
 

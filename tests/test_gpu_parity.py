@@ -242,6 +242,13 @@ LOSS_CASES = [
     ("kl_k1_f32", "f32", 4096, [20, 11], {"kl_beta": 0.1, "kl_mode": 1}, {}),
     ("kl_k2_bf16", "bf16", 32000, [17, 9], {"kl_beta": 0.1, "kl_mode": 2}, {}),
     ("kl_abs_bf16_odd", "bf16", 20011, [13, 15], {"kl_beta": 0.1, "kl_mode": 3}, {}),
+    # vocab-parallel shard widths (P = 8 / 4 of Qwen3): the row-stream kernels (4 / 2 streams),
+    # row counts that leave the last group of a CTA partial
+    ("vp8_shard_bf16_streams4", "bf16", 18992, [40, 33, 17, 9, 51], {}, {}),
+    ("vp4_shard_kl_ent_streams2", "bf16", 37984, [30, 21, 7], {"kl_beta": 0.05, "entropy_coef": 0.01}, {}),
+    ("vp8_shard_f32_streams2", "f32", 18992, [19, 23, 5], {"kl_beta": 0.05}, {}),
+    ("vp8_shard_inplace", "bf16", 18992, [21, 14], {}, {"in_place": True}),
+    ("vp8_shard_masked_skip", "bf16", 18992, [17, 30, 2], {}, {"masked_skip": True}),
 ]
 
 
@@ -305,7 +312,8 @@ def test_pg_loss_deep_runahead(tm, orc, dtype, V):
     check_loss_case(tm, orc, prob)
 
 
-@pytest.mark.parametrize("dtype,T,V", [("bf16", 20000, 151936), ("bf16", 8000, 75968), ("f32", 5000, 16000)])
+@pytest.mark.parametrize("dtype,T,V", [("bf16", 20000, 151936), ("bf16", 8000, 75968), ("f32", 5000, 16000),
+                                       ("bf16", 9001, 18992), ("bf16", 6007, 37984)])
 def test_fused_all_rows_vs_streaming_forward(tm, dtype, T, V):
     """Race regression: every loss-active row's logp/entropy from the fused
     kernel equals the streaming forward kernel's, over repeated launches at
@@ -321,9 +329,14 @@ def test_fused_all_rows_vs_streaming_forward(tm, dtype, T, V):
     w = (torch.rand(T, generator=g) < 0.8).float().cuda() / T
     lp_ref, ent_ref, _ = tm.logprob_fwd(lg, tg)
     act = w != 0
+    # row streams by shard width (SFTM_LOSS_NS unset): 4 at 18,992 bf16, 2 at 37,984 bf16 / 16,000 f32
+    want_ns = {18992: 4, 37984: 2, 16000: 2}.get(V, 1)
     for _ in range(4):
         _, _, lp, ent = tm.pg_loss_fwd_bwd(lg, tg, o, r, a, w, want_logp=True)
         torch.cuda.synchronize()
+        env = __import__("os").environ
+        if "SFTM_LOSS_NS" not in env and "SFTM_LOSS_C" not in env:
+            assert tm.handle().last_launch()["streams"] == want_ns
         bad = ((lp - lp_ref).abs() > 2e-5 + 2e-6 * lp_ref.abs()) & act
         bad |= ((ent - ent_ref).abs() > 2e-5 + 2e-5 * ent_ref.abs()) & act
         assert int(bad.sum()) == 0, f"{int(bad.sum())} rows differ, e.g. {torch.nonzero(bad)[:5].flatten().tolist()}"
@@ -611,6 +624,25 @@ def test_full_vocab_large_batch_properties(tm, orc):
     # metrics self-consistency: recompute sum w*H from per-row outputs
     wh = float((w_tok.double() * ent.double()).sum())
     assert abs(met[3].item() - wh) <= 1e-5 * abs(wh) + 1e-6
+
+
+@pytest.mark.parametrize("NS", [1, 2, 4])
+def test_row_stream_count_parity(NS):
+    """Every row-stream count of the fused kernel (SFTM_LOSS_NS forces one where
+    a row fits; the default picks by width) meets the same parity bar on the
+    loss cases, the deep run-ahead cases (many one-chunk rows, partial last
+    groups) and the all-rows race regression."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SFTM_LOSS_NS=str(NS))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_parity.py", "-k",
+                          "test_pg_loss_fwd_bwd or deep_runahead or all_rows or neg_inf",
+                          "--timeout", "120"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
 @pytest.mark.parametrize("C", [2, 3, 4])
