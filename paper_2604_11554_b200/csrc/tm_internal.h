@@ -67,7 +67,10 @@ struct RowArgs {
 // than the row's HBM time at narrow shards).
 constexpr int kXpMaxP = 8;
 constexpr int kXpMaxCtas = 256;
-constexpr int kXpMailD = 16;
+#ifndef SFTM_XP_MAILD
+#define SFTM_XP_MAILD 16
+#endif
+constexpr int kXpMailD = SFTM_XP_MAILD;
 struct alignas(32) XpMsg {
   unsigned long long w[4];
 };

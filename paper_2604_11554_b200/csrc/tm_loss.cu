@@ -87,13 +87,15 @@ constexpr int kRD = SFTM_RD;                      // depth of the per-row partia
 // red/scal rings bounded, a CTA's control warp is at most 2*kRD+1 rows ahead
 // of its partner's mailbox reads, so 16 can never be overrun.
 constexpr int kMailD = 16;
-static_assert(kMailD == kXpMailD, "peer mailbox ring depth must match the cluster mailbox ring");
 // XP sender credit: the sender posts row n only after its receiver finished
-// row n - kXpCredit. Then a rank posting row n into a peer's slot n % kMailD
-// implies that peer's receiver finished row n - 2*kXpCredit >= n - kMailD.
-constexpr int kXpCredit = 6;
-constexpr int kCredD = 8;
-static_assert(2 * kXpCredit <= kMailD && kXpCredit < kCredD, "credit bounds");
+// row n - kXpCredit. Then a rank posting row n into a peer's slot n % kXpMailD
+// implies that peer's receiver finished row n - 2*kXpCredit >= n - kXpMailD.
+#ifndef SFTM_XP_CREDIT
+#define SFTM_XP_CREDIT 6
+#endif
+constexpr int kXpCredit = SFTM_XP_CREDIT;
+constexpr int kCredD = kXpCredit + 2;
+static_assert(2 * kXpCredit <= kXpMailD && kXpCredit < kCredD, "credit bounds");
 
 // Per-row scalars computed once by the control warp and broadcast in smem.
 struct RowScal {
@@ -240,6 +242,44 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // vocab-parallel shard at P = 4 / 8). Streams advance in lockstep: the NS rows
 // of a group have the same width, and a stream with no row in the CTA's last
 // group idles through its steps.
+// Warp-collective walk over a CTA's rows t = cid + n * ncl (n = 0, 1, ...)
+// yielding the loss-active ones (w_tok != 0): 32 rows per ballot over their
+// weights, the next window's weights loaded one window ahead, so finding the
+// next active row costs no dependent global load. Every lane gets the same rows.
+struct RowWalk {
+  const float* w;
+  int64_t T, cid, ncl, win;
+  uint32_t act;  // active rows of the current window not yet returned
+  float wnext;   // this lane's row weight in the next window
+  int lane;
+  __device__ __forceinline__ float load(int64_t wi) const {
+    const int64_t t = cid + (32 * wi + lane) * ncl;
+    return t < T ? __ldg(w + t) : 0.f;
+  }
+  __device__ __forceinline__ void init(const float* w_, int64_t T_, int64_t cid_, int64_t ncl_, int lane_) {
+    w = w_;
+    T = T_;
+    cid = cid_;
+    ncl = ncl_;
+    lane = lane_;
+    win = 0;
+    act = __ballot_sync(0xffffffffu, load(0) != 0.f);
+    wnext = load(1);
+  }
+  __device__ __forceinline__ bool next(int64_t& t) {
+    while (act == 0u) {
+      if (cid + 32 * (win + 1) * ncl >= T) return false;
+      ++win;
+      act = __ballot_sync(0xffffffffu, wnext != 0.f);
+      wnext = load(win + 1);
+    }
+    const int i = __ffs(act) - 1;
+    act &= act - 1u;
+    t = cid + (32 * win + i) * ncl;
+    return true;
+  }
+};
+
 #ifdef SFTM_HANG_DEBUG
 // Debug build only (EXTRA=-DSFTM_HANG_DEBUG, scripts/hang_debug.py): a wait that
 // gives up after 2 s and records where, so a protocol deadlock shows its
@@ -296,8 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[kSlots];
   __shared__ __align__(8) uint64_t tfull_bar[kStore];
   __shared__ __align__(8) uint64_t tempty_bar[kStore];
-  __shared__ __align__(8) uint64_t mail_bar[kMailD];
-  __shared__ __align__(16) float4 mail[kMailD][8];
+  constexpr int kMB = (C > 1) ? kMailD : 1;  // cluster mailboxes (C == 1 exchanges nothing in smem)
+  __shared__ __align__(8) uint64_t mail_bar[kMB];
+  __shared__ __align__(16) float4 mail[kMB][8];
   __shared__ __align__(16) float4 red[RD][SW];       // per forward warp of the row's stream: (m2, s, w, -)
   __shared__ __align__(8) uint64_t red_bar[RD], red_free[RD];
   __shared__ __align__(16) RowScal scal[RD];
@@ -331,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&tfull_bar[i]), kFT);
       mbar_init(smem_u32(&tempty_bar[i]), kFT);  // backward threads (same count)
     }
-    for (int i = 0; i < kMailD; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
+    for (int i = 0; i < kMB; ++i) mbar_init(smem_u32(&mail_bar[i]), C);
     for (int i = 0; i < RD; ++i) {
       mbar_init(smem_u32(&red_bar[i]), SW);   // lane 0 of each forward warp of the row's stream
       mbar_init(smem_u32(&red_free[i]), 1);   // lane 0 of the control warp that read it
@@ -397,38 +438,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kProd) {
     // ================================================================ producer
-    if (NS > 1 && lane == 0) {
-      // row streams: a group of up to NS loss-active rows, one per stream;
-      // slot step k carries sub-chunk k of every row of the group
+    if (NS > 1) {
+      // Row streams: a group of up to NS loss-active rows, one per stream;
+      // slot step k carries sub-chunk k of every row of the group, copied by
+      // lane g for stream g. The whole warp runs the loop: loss-active rows
+      // are found 32 at a time by a ballot over their weights (loaded one
+      // window ahead), and the NS copies of a step share one call site. With
+      // a lane-0 loop and one row weight per iteration (one dependent load per
+      // row) and a 64-bit address setup per copy, the producer needed ~120
+      // instructions per step at ~0.1 IPC and starved 4 streams.
       const uint64_t pol = l2_evict_first_policy();
       uint32_t slot = 0, ph = 0;
-      int64_t grow[NS];
+      RowWalk rw;
+      rw.init(a.w_tok, a.T, cid, ncl, lane);
+      const char* my_src = nullptr;  // lane g < NS: stream g's row of the current group
       int ng = 0;
       auto issue_group = [&]() {
         for (int k = 0; k < nck; ++k) {
           const int rem = slice_len - k * SCE;
           const uint32_t bytes = static_cast<uint32_t>(rem < SCE ? rem : SCE) * G::es;
           DBG_WAIT(w_a, KWAIT(smem_u32(&empty_bar[slot]), ph ^ 1u));
-          mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes * static_cast<uint32_t>(ng));
-#pragma unroll
-          for (int g = 0; g < NS; ++g)
-            if (g < ng)
-              bulk_g2s(ring_base + slot * kCB + g * SCB, logits + grow[g] * a.ld + static_cast<int64_t>(k) * SCE,
-                       bytes, smem_u32(&full_bar[slot]), pol);
+          if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes * static_cast<uint32_t>(ng));
+          __syncwarp();
+          if (lane < ng)
+            bulk_g2s(ring_base + slot * kCB + lane * SCB, my_src + static_cast<int64_t>(k) * SCB, bytes,
+                     smem_u32(&full_bar[slot]), pol);
           if (++slot == kSlots) {
             slot = 0;
             ph ^= 1u;
           }
         }
       };
-      float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
-      for (int64_t t = cid; t < a.T; t += ncl) {
-        const float wcur = wn;
-        if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
-        if (wcur == 0.f) continue;
-#pragma unroll
-        for (int g = 0; g < NS; ++g)
-          if (g == ng) grow[g] = t;  // register-resident (no dynamic index)
+      int64_t t;
+      while (rw.next(t)) {
+        if (lane == ng) my_src = reinterpret_cast<const char*>(logits + t * a.ld);
         if (++ng == NS) {
           issue_group();
           ng = 0;
@@ -789,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-        const uint32_t mb = nrow % kMailD;
+        const uint32_t mb = nrow % kXpMailD;
         const uint64_t tag = static_cast<uint64_t>(static_cast<uint32_t>(a.xp_epoch << 20) + nrow + 1u) << 32;
         const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
         if (ci == 0) {
@@ -955,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         st = stats_merge(st, v);  // one CTA per row: no exchange
       } else {
         const float z = 0.f;
-        const uint32_t mb = nrow % kMailD;
+        const uint32_t mb = nrow % kXpMailD;
         if (lane == 0) {
           const uint32_t my_slot = smem_u32(&mail[mb][crank]);
           const uint32_t my_bar = smem_u32(&mail_bar[mb]);
