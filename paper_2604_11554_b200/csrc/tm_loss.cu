@@ -242,6 +242,33 @@ __device__ __forceinline__ void store_vec(uint16_t* p, const float* g) {
 // vocab-parallel shard at P = 4 / 8). Streams advance in lockstep: the NS rows
 // of a group have the same width, and a stream with no row in the CTA's last
 // group idles through its steps.
+// A control warp's per-row inputs, one row per lane of a 32-row window of the
+// CTA's rows (rows cid + (32 * win + lane) * ncl); loaded a window ahead, a
+// row's inputs are then one shuffle away instead of a dependent load per row.
+struct RowIn {
+  float w, A, old, ref;
+  int32_t y;
+};
+__device__ __forceinline__ RowIn load_row_in(const RowArgs& a, int64_t cid, int64_t ncl, int64_t win, int lane) {
+  RowIn r{0.f, 0.f, 0.f, 0.f, 0};
+  const int64_t t = cid + (32 * win + lane) * ncl;
+  if (t < a.T) {
+    r.w = __ldg(a.w_tok + t);
+    r.A = __ldg(a.adv_tok + t);
+    r.old = __ldg(a.old_logp + t);
+    r.ref = __ldg(a.ref_logp + t);
+    r.y = __ldg(a.targets + t);
+  }
+  return r;
+}
+// masked rows get logp = entropy = 0 (each lane its own row of the window)
+__device__ __forceinline__ void zero_masked_outputs(const RowArgs& a, int64_t t, float w) {
+  if (t < a.T && w == 0.f) {
+    if (a.out_logp) a.out_logp[t] = 0.f;
+    if (a.out_entropy) a.out_entropy[t] = 0.f;
+  }
+}
+
 // Warp-collective walk over a CTA's rows t = cid + n * ncl (n = 0, 1, ...)
 // yielding the loss-active ones (w_tok != 0): 32 rows per ballot over their
 // weights, the next window's weights loaded one window ahead, so finding the
@@ -250,8 +277,10 @@ struct RowWalk {
   const float* w;
   int64_t T, cid, ncl, win;
   uint32_t act;  // active rows of the current window not yet returned
+  uint32_t msk;  // masked rows (w == 0) of the current window not yet returned (next_all)
   float wnext;   // this lane's row weight in the next window
   int lane;
+  __device__ __forceinline__ bool exists(int64_t wi) const { return cid + (32 * wi + lane) * ncl < T; }
   __device__ __forceinline__ float load(int64_t wi) const {
     const int64_t t = cid + (32 * wi + lane) * ncl;
     return t < T ? __ldg(w + t) : 0.f;
@@ -263,20 +292,82 @@ struct RowWalk {
     ncl = ncl_;
     lane = lane_;
     win = 0;
-    act = __ballot_sync(0xffffffffu, load(0) != 0.f);
+    const float w0 = load(0);
+    act = __ballot_sync(0xffffffffu, w0 != 0.f);
+    msk = __ballot_sync(0xffffffffu, exists(0) && w0 == 0.f);
     wnext = load(1);
   }
+  __device__ __forceinline__ bool advance() {
+    if (cid + 32 * (win + 1) * ncl >= T) return false;
+    ++win;
+    act = __ballot_sync(0xffffffffu, wnext != 0.f);
+    msk = __ballot_sync(0xffffffffu, exists(win) && wnext == 0.f);
+    wnext = load(win + 1);
+    return true;
+  }
+  // every row in order, loss-active or not (the backward zero-fills masked rows)
+  __device__ __forceinline__ bool next_all(int64_t& t, bool& active) {
+    while ((act | msk) == 0u)
+      if (!advance()) return false;
+    const int i = __ffs(act | msk) - 1;
+    active = (act >> i) & 1u;
+    act &= ~(1u << i);
+    msk &= ~(1u << i);
+    t = cid + (32 * win + i) * ncl;
+    return true;
+  }
   __device__ __forceinline__ bool next(int64_t& t) {
-    while (act == 0u) {
-      if (cid + 32 * (win + 1) * ncl >= T) return false;
-      ++win;
-      act = __ballot_sync(0xffffffffu, wnext != 0.f);
-      wnext = load(win + 1);
-    }
+    while (act == 0u)
+      if (!advance()) return false;
     const int i = __ffs(act) - 1;
     act &= act - 1u;
     t = cid + (32 * win + i) * ncl;
     return true;
+  }
+};
+
+// The loss-active rows of a CTA in order (and, with next_all, the masked
+// ones too). Row streams (NS > 1) skip most rows, so they find them with the
+// ballot walk; one row at a time (NS == 1), the next row's weight loaded a row
+// ahead by each thread is as fast and measured cheaper at wide rows.
+template <int NS>
+struct RowSeq {
+  RowWalk rw;
+  const float* w;
+  int64_t T, ncl, t;
+  float wn;
+  __device__ __forceinline__ void init(const float* w_, int64_t T_, int64_t cid, int64_t ncl_, int lane) {
+    if constexpr (NS > 1) {
+      rw.init(w_, T_, cid, ncl_, lane);
+    } else {
+      w = w_;
+      T = T_;
+      ncl = ncl_;
+      t = cid - ncl_;
+      wn = (cid < T_) ? __ldg(w_ + cid) : 0.f;
+    }
+  }
+  __device__ __forceinline__ bool next_all(int64_t& row, bool& active) {
+    if constexpr (NS > 1) {
+      return rw.next_all(row, active);
+    } else {
+      t += ncl;
+      if (t >= T) return false;
+      active = wn != 0.f;
+      if (t + ncl < T) wn = __ldg(w + t + ncl);
+      row = t;
+      return true;
+    }
+  }
+  __device__ __forceinline__ bool next(int64_t& row) {
+    if constexpr (NS > 1) {
+      return rw.next(row);
+    } else {
+      bool active = false;
+      while (next_all(row, active))
+        if (active) return true;
+      return false;
+    }
   }
 };
 
@@ -479,9 +570,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (ng > 0) issue_group();
     } else if (lane == 0) {
+      // one row at a time (one copy per step): lane 0 alone, the next row's
+      // weight loaded a row ahead (measured faster than the warp-wide walk here)
       const uint64_t pol = l2_evict_first_policy();
       uint32_t slot = 0, ph = 0;
-      float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;  // next row's weight, one row ahead
+      float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
       for (int64_t t = cid; t < a.T; t += ncl) {
         const float wcur = wn;
         if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
@@ -565,12 +658,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tph ^= 1u;
       }
     };
-    // the row weight is loaded one row ahead so its latency never sits on the row boundary
-    float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
-    for (int64_t t = cid; t < a.T; t += ncl) {
-      const float wcur = wn;
-      if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
-      if (wcur == 0.f) continue;
+    RowSeq<NS> rows;
+    rows.init(a.w_tok, a.T, cid, ncl, lane);
+    int64_t t;
+    while (rows.next(t)) {
       if (NS > 1 && static_cast<int>(nrow % NS) != sg) {  // another stream's row
         ++nrow;
         continue;
@@ -801,37 +892,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the same bound on every rank keeps any rank from overrunning a peer's
       // kMailD-deep mailbox ring.
       uint32_t nrow = 0;
-      float wn = 0.f, An = 0.f, oldn = 0.f, refn = 0.f;
-      int32_t yn = 0;
-      if (cid < a.T) {
-        wn = __ldg(a.w_tok + cid);
-        yn = __ldg(a.targets + cid);
-        if (ci >= 1) {
-          An = __ldg(a.adv_tok + cid);
-          oldn = __ldg(a.old_logp + cid);
-          refn = __ldg(a.ref_logp + cid);
-        }
-      }
-      for (int64_t t = cid; t < a.T; t += ncl) {
-        const float w = wn, A = An, old = oldn, ref = refn;
-        const int32_t ycur = yn;
-        if (t + ncl < a.T) {
-          const int64_t tn = t + ncl;
-          wn = __ldg(a.w_tok + tn);
-          yn = __ldg(a.targets + tn);
-          if (ci >= 1) {
-            An = __ldg(a.adv_tok + tn);
-            oldn = __ldg(a.old_logp + tn);
-            refn = __ldg(a.ref_logp + tn);
-          }
-        }
-        if (w == 0.f) {
-          if (leader && ci == 0) {
-            if (a.out_logp) a.out_logp[t] = 0.f;
-            if (a.out_entropy) a.out_entropy[t] = 0.f;
-          }
-          continue;
-        }
+      RowIn nx = load_row_in(a, cid, ncl, 0, lane);
+      for (int64_t win = 0; cid + 32 * win * ncl < a.T; ++win) {
+        const RowIn cur = nx;
+        nx = load_row_in(a, cid, ncl, win + 1, lane);  // one window ahead
+        const int64_t tl = cid + (32 * win + lane) * ncl;  // this lane's row of the window
+        if (ci == 0) zero_masked_outputs(a, tl, cur.w);
+        uint32_t bits = __ballot_sync(0xffffffffu, tl < a.T && cur.w != 0.f);
+        while (bits != 0u) {
+        const int i = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const int64_t t = cid + (32 * win + i) * ncl;
+        const float w = __shfl_sync(0xffffffffu, cur.w, i), A = __shfl_sync(0xffffffffu, cur.A, i);
+        const float old = __shfl_sync(0xffffffffu, cur.old, i), ref = __shfl_sync(0xffffffffu, cur.ref, i);
+        const int32_t ycur = __shfl_sync(0xffffffffu, cur.y, i);
         const uint32_t mb = nrow % kXpMailD;
         const uint64_t tag = static_cast<uint64_t>(static_cast<uint32_t>(a.xp_epoch << 20) + nrow + 1u) << 32;
         const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
@@ -933,40 +1007,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         ++nrow;
+        }
       }
     } else {
     uint32_t nrow = 0;
-    float wn = 0.f, An = 0.f, oldn = 0.f, refn = 0.f;
-    int32_t yn = 0;
-    if (cid < a.T) {
-      wn = __ldg(a.w_tok + cid);
-      An = __ldg(a.adv_tok + cid);
-      oldn = __ldg(a.old_logp + cid);
-      refn = __ldg(a.ref_logp + cid);
-      yn = __ldg(a.targets + cid);
-    }
-    for (int64_t t = cid; t < a.T; t += ncl) {
-      const float w = wn, A = An, old = oldn, ref = refn;
-      const int32_t ycur = yn;
-      if (t + ncl < a.T) {  // next row's inputs, one row ahead
-        const int64_t tn = t + ncl;
-        wn = __ldg(a.w_tok + tn);
-        An = __ldg(a.adv_tok + tn);
-        oldn = __ldg(a.old_logp + tn);
-        refn = __ldg(a.ref_logp + tn);
-        yn = __ldg(a.targets + tn);
-      }
-      if (w == 0.f) {
-        if (leader && ci == 0) {
-          if (a.out_logp) a.out_logp[t] = 0.f;
-          if (a.out_entropy) a.out_entropy[t] = 0.f;
-        }
-        continue;
-      }
-      if (static_cast<int>(nrow % kNCtl) != ci) {  // the other control warp's row
+    RowIn nx = load_row_in(a, cid, ncl, 0, lane);
+    for (int64_t win = 0; cid + 32 * win * ncl < a.T; ++win) {
+      const RowIn cur = nx;
+      nx = load_row_in(a, cid, ncl, win + 1, lane);  // one window ahead
+      const int64_t tl = cid + (32 * win + lane) * ncl;  // this lane's row of the window
+      if (ci == 0 && crank == 0) zero_masked_outputs(a, tl, cur.w);
+      uint32_t bits = __ballot_sync(0xffffffffu, tl < a.T && cur.w != 0.f);
+      // rows of the other control warps
+      while (bits != 0u && static_cast<int>(nrow % kNCtl) != ci) {
+        bits &= bits - 1u;
         ++nrow;
-        continue;
       }
+      while (bits != 0u) {
+      const int i = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      const int64_t t = cid + (32 * win + i) * ncl;
+      const float w = __shfl_sync(0xffffffffu, cur.w, i), A = __shfl_sync(0xffffffffu, cur.A, i);
+      const float old = __shfl_sync(0xffffffffu, cur.old, i), ref = __shfl_sync(0xffffffffu, cur.ref, i);
+      const int32_t ycur = __shfl_sync(0xffffffffu, cur.y, i);
       const uint32_t rs = nrow % RD;
       const uint32_t rpar = (nrow / RD) & 1u;
       const int64_t yg = static_cast<int64_t>(ycur) - a.vocab_start;
@@ -1049,6 +1112,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     
       ++nrow;
+      // skip to this warp's next row (kNCtl - 1 rows of the other control warps)
+      for (int q = 1; q < kNCtl && bits != 0u; ++q) {
+        bits &= bits - 1u;
+        ++nrow;
+      }
+      }
+      // rows of this window past our last one belong to the others: nrow already
+      // counts every row handed out above
     }
     }  // XP / alternating
     // fixed-order combine of the two control warps' fp64 partials, then the
@@ -1079,11 +1150,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t stash_t = stash_base + 16u * btid;
     const uint32_t sink_a = smem_u32(&sink_sh[warp]);  // dummy-store target (never read)
     uint32_t ts = 0, tph = 0, nrow = 0;
-    float wn = (cid < a.T) ? __ldg(a.w_tok + cid) : 0.f;
-    for (int64_t t = cid; t < a.T; t += ncl) {
-      const float w = wn;
-      if (t + ncl < a.T) wn = __ldg(a.w_tok + t + ncl);
-      if (w == 0.f) {
+    RowSeq<NS> rows;
+    rows.init(a.w_tok, a.T, cid, ncl, lane);
+    int64_t t;
+    bool active;
+    while (rows.next_all(t, active)) {
+      if (!active) {
         if (!a.masked_skip) {
           T* drow0 = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start;
           if constexpr (UA) {
