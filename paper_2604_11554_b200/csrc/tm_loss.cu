@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int dbg_mode = SFTM_DBG_MODE;
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
   static_assert(!UA || (C == 1 && !XP), "unaligned rows run one CTA per row");
-  static_assert(NS == 1 || (C == 1 && !UA), "row streams: one CTA per row slice, aligned rows");
+  static_assert(NS == 1 || C == 1, "row streams: one CTA per row slice");
   static_assert(NS == 1 || NS == 2 || NS == 4, "row streams");
   using G = Geo<T>;
   constexpr int CE = G::CE;
@@ -451,6 +451,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int slice_len = static_cast<int>(sl64);
   const int nck = (slice_len + SCE - 1) / SCE;
   const int nfull = slice_len / SCE;
+  // slot steps per group of rows: unaligned rows start up to EV - 1 elements
+  // into their first sub-chunk, so a group takes the most any row can need and
+  // a row with fewer chunks idles the rest
+  const int nstep = UA ? (slice_len + EV - 1 + SCE - 1) / SCE : nck;
   const uint32_t ring_base = smem_u32(ring);
   const uint32_t stash_base = ring_base + kSlots * kCB;  // smem row-store slot i = store slot kTSlots + i
 
@@ -542,17 +546,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t slot = 0, ph = 0;
       RowWalk rw;
       rw.init(a.w_tok, a.T, cid, ncl, lane);
-      const char* my_src = nullptr;  // lane g < NS: stream g's row of the current group
+      const T* my_row = nullptr;  // lane g < NS: stream g's row of the current group (sector start if UA)
+      int my_span = 0;            // ... its extent in sector coordinates
+      int64_t my_t = -1;
       int ng = 0;
       auto issue_group = [&]() {
-        for (int k = 0; k < nck; ++k) {
-          const int rem = slice_len - k * SCE;
-          const uint32_t bytes = static_cast<uint32_t>(rem < SCE ? rem : SCE) * G::es;
+        for (int k = 0; k < nstep; ++k) {
+          const int rem = my_span - k * SCE;
+          uint32_t bytes = (lane < ng && rem > 0) ? static_cast<uint32_t>(rem < SCE ? rem : SCE) * G::es : 0u;
+          int tail = 0;  // UA: elements of the tensor's final partial sector, loaded by this lane
+          if constexpr (UA) {
+            if ((bytes & 15u) && my_t == a.T - 1 && rem <= SCE) {
+              tail = static_cast<int>((bytes & 15u) / G::es);  // never read past the tensor
+              bytes &= ~15u;
+            } else {
+              bytes = (bytes + 15u) & ~15u;  // whole sectors (inside the tensor)
+            }
+          }
+          const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);  // the step's TMA bytes
           DBG_WAIT(w_a, KWAIT(smem_u32(&empty_bar[slot]), ph ^ 1u));
-          if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), bytes * static_cast<uint32_t>(ng));
+          if constexpr (UA) {
+            if (tail) {
+              const T* tp = my_row + static_cast<int64_t>(k) * SCE + bytes / G::es;
+              T* ts_ = reinterpret_cast<T*>(ring + slot * kCB + lane * SCB + bytes);
+              for (int j = 0; j < tail; ++j) ts_[j] = tp[j];
+              __threadfence_block();  // ordered before lane 0's release arrive (after the warp sync)
+            }
+          }
           __syncwarp();
-          if (lane < ng)
-            bulk_g2s(ring_base + slot * kCB + lane * SCB, my_src + static_cast<int64_t>(k) * SCB, bytes,
+          if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full_bar[slot]), total);
+          __syncwarp();
+          if (bytes)
+            bulk_g2s(ring_base + slot * kCB + lane * SCB, my_row + static_cast<int64_t>(k) * SCE, bytes,
                      smem_u32(&full_bar[slot]), pol);
           if (++slot == kSlots) {
             slot = 0;
@@ -562,13 +587,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       int64_t t;
       while (rw.next(t)) {
-        if (lane == ng) my_src = reinterpret_cast<const char*>(logits + t * a.ld);
+        if (lane == ng) {
+          const int mis = row_mis(t);
+          my_row = logits + t * a.ld + slice_start - mis;
+          my_span = slice_len + mis;
+          my_t = t;
+        }
         if (++ng == NS) {
           issue_group();
           ng = 0;
         }
       }
-      if (ng > 0) issue_group();
+      if (ng > 0) {
+        if (lane >= ng) my_span = 0;  // streams with no row in the last group
+        issue_group();
+      }
     } else if (lane == 0) {
       // one row at a time (one copy per step): lane 0 alone, the next row's
       // weight loaded a row ahead (measured faster than the warp-wide walk here)
@@ -581,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wcur == 0.f) continue;
         const int mis = row_mis(t);
         const int span = slice_len + mis;
-        const int nck_r = UA ? (span + CE - 1) / CE : nck;
+        const int nck_r = UA ? (span + SCE - 1) / SCE : nck;
         const T* row = logits + t * a.ld + slice_start - mis;
         for (int k = 0; k < nck_r; ++k) {
           const int rem = span - k * SCE;
@@ -668,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int mis = row_mis(t);
       const int span = slice_len + mis;  // row extent in sector coordinates
-      const int nck_r = UA ? (span + CE - 1) / CE : nck;
+      const int nck_r = UA ? (span + SCE - 1) / SCE : nck;
       float m2 = 0.f;
       // two float2 partial sums = 4 independent chains, updated with FADD2/FFMA2
       float2 s2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -793,9 +826,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       if constexpr (UA) {
         // peeled like the aligned schedule: only the front and tail chunks are masked
-        const int nfull_r = span / CE;
+        const int nfull_r = span / SCE;
         if (nck_r > 0) {
-          if (mis > 0 || span < CE) {
+          if (mis > 0 || span < SCE) {
             chunk(0, true, true);
           } else {
             chunk(0, true, false);
@@ -803,6 +836,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 1; k < nfull_r; ++k) chunk(k, false, false);
           if (nck_r > nfull_r && nck_r > 1) chunk(nck_r - 1, false, true);
         }
+        if (NS > 1)
+          for (int k = nck_r; k < nstep; ++k) fidle();  // the group's longer rows still stream
       } else if (nck == 0) {
         // empty slice (a cluster wider than the vocab): contributes nothing
       } else if (nfull == 0) {
@@ -869,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // the CTA's last group of rows has no row for this stream: idle through its steps
     if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS))
-      for (int k = 0; k < nck; ++k) fidle();
+      for (int k = 0; k < nstep; ++k) fidle();
   } else if (warp >= kCtl) {
     // ================================================================ control
     // Per row: merge the 12 forward partials, exchange with the cluster through
@@ -1182,7 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int mis = row_mis(t);
       const int span = slice_len + mis;  // row extent in sector coordinates
-      const int nck_r = UA ? (span + CE - 1) / CE : nck;
+      const int nck_r = UA ? (span + SCE - 1) / SCE : nck;
       const uint32_t rs = nrow % RD;
       const uint32_t rpar = (nrow / RD) & 1u;
       DBG_WAIT(w_a, KWAIT(smem_u32(&scal_bar[rs]), rpar));
@@ -1379,8 +1414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
       if constexpr (UA) {
-        const int nfull_r = span / CE;
-        const bool front = mis > 0 || span < CE;
+        const int nfull_r = span / SCE;
+        const bool front = mis > 0 || span < SCE;
         auto sched = [&](auto md) {
           constexpr int M = decltype(md)::value;
           if (nck_r == 0) return;
@@ -1409,6 +1444,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < nfull; ++k) bchunk(k, false, 2);
         if (nck > nfull) bchunk(nfull, true, 2);
       }
+      if (UA && NS > 1) {
+        for (int k = nck_r; k < nstep; ++k) {  // the group's longer rows still stream
+          DBG_WAIT(w_b, KWAIT(tfull0 + 8u * ts, tph));
+          mbar_arrive(tempty0 + 8u * ts);
+          if (++ts == kStore) {
+            ts = 0;
+            tph ^= 1u;
+          }
+        }
+      }
       // the row's stores consumed every lane's scalars (a row with no chunk
       // here consumes them through a dependent dummy smem store): free the slot
       if (nck_r == 0) sink_u32(sink_a, __float_as_uint(lse2f) ^ __float_as_uint(c0) ^ rsc.sgn ^ rsc.town);
@@ -1418,7 +1463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // the CTA's last group of rows has no row for this stream: idle through its steps
     if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS)) {
-      for (int k = 0; k < nck; ++k) {
+      for (int k = 0; k < nstep; ++k) {
         DBG_WAIT(w_b, KWAIT(tfull0 + 8u * ts, tph));
         mbar_arrive(tempty0 + 8u * ts);  // nothing read from the row-store slot
         if (++ts == kStore) {
@@ -1570,7 +1615,11 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
   if (ua) {
     if ((a.V + G::EV - 1 + G::CE - 1) / G::CE > kMaxChunks) return -2;
-    return launch_c<T, 1, false, true>(a, a.V, s, info);
+    switch (pick_streams<T>(a.V + G::EV - 1)) {  // a row spans up to EV - 1 more elements
+      case 4: return launch_c<T, 1, false, true, 4>(a, a.V, s, info);
+      case 2: return launch_c<T, 1, false, true, 2>(a, a.V, s, info);
+    }
+    return launch_c<T, 1, false, true, 1>(a, a.V, s, info);
   }
   static const int forced = [] {  // tuning knob: SFTM_LOSS_C=1|2|3|4|8
     const char* v = getenv("SFTM_LOSS_C");

@@ -249,6 +249,11 @@ LOSS_CASES = [
     ("vp8_shard_f32_streams2", "f32", 18992, [19, 23, 5], {"kl_beta": 0.05}, {}),
     ("vp8_shard_inplace", "bf16", 18992, [21, 14], {}, {"in_place": True}),
     ("vp8_shard_masked_skip", "bf16", 18992, [17, 30, 2], {}, {"masked_skip": True}),
+    # unaligned rows (16-B sector coordinates) through the row streams: each row of a
+    # group has its own sector phase, so rows of one group take different chunk counts
+    ("odd_shard_bf16_streams4", "bf16", 18993, [30, 27, 11], {"entropy_coef": 0.01}, {}),
+    ("odd_32001_bf16_streams2_inplace", "bf16", 32001, [14, 23], {}, {"in_place": True}),
+    ("odd_9497_f32_streams2_skip", "f32", 9497, [19, 8, 25], {"kl_beta": 0.05}, {"masked_skip": True}),
 ]
 
 
@@ -313,7 +318,7 @@ def test_pg_loss_deep_runahead(tm, orc, dtype, V):
 
 
 @pytest.mark.parametrize("dtype,T,V", [("bf16", 20000, 151936), ("bf16", 8000, 75968), ("f32", 5000, 16000),
-                                       ("bf16", 9001, 18992), ("bf16", 6007, 37984)])
+                                       ("bf16", 9001, 18992), ("bf16", 6007, 37984), ("bf16", 7001, 18993)])
 def test_fused_all_rows_vs_streaming_forward(tm, dtype, T, V):
     """Race regression: every loss-active row's logp/entropy from the fused
     kernel equals the streaming forward kernel's, over repeated launches at
@@ -330,7 +335,7 @@ def test_fused_all_rows_vs_streaming_forward(tm, dtype, T, V):
     lp_ref, ent_ref, _ = tm.logprob_fwd(lg, tg)
     act = w != 0
     # row streams by shard width (SFTM_LOSS_NS unset): 4 at 18,992 bf16, 2 at 37,984 bf16 / 16,000 f32
-    want_ns = {18992: 4, 37984: 2, 16000: 2}.get(V, 1)
+    want_ns = {18992: 4, 37984: 2, 16000: 2, 18993: 4}.get(V, 1)
     for _ in range(4):
         _, _, lp, ent = tm.pg_loss_fwd_bwd(lg, tg, o, r, a, w, want_logp=True)
         torch.cuda.synchronize()
