@@ -1560,27 +1560,34 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
   return e;
 }
 
-// Row streams for a one-CTA row slice of `slice` elements: the most streams
-// whose per-stream row still leaves the row store room for two rows (so the
-// forward of one group overlaps the backward of the previous one).
+// Row streams for a one-CTA row slice of `slice` elements (for unaligned rows
+// the widest span, V + EV - 1). Measured on B200 (scripts/ns_ab.sh, bf16): the
+// most streams whose per-stream row takes <= 15 sub-chunks, i.e. leaves the
+// row store room for two groups of rows (18,992 wide -> 4, 24,576 / 27,648 /
+// 37,984 -> 2); at 16-18 sub-chunks the store holds < 2 groups and the
+// pipeline stalls (24,576 at 4 streams, 55,296 at 2: 3-8% slower), unless one
+// row at a time wastes a large part of its last chunk or handles unaligned
+// rows (50,256: +2.5%, 50,257: +14% at 17 sub-chunks and 2 streams).
 // SFTM_LOSS_NS=1|2|4 forces a count (tuning, tests).
 template <typename T>
-int pick_streams(int64_t slice) {
+int pick_streams(int64_t slice, bool ua) {
   using G = Geo<T>;
   static const int forced = [] {
     const char* v = getenv("SFTM_LOSS_NS");
     return v ? atoi(v) : 0;
   }();
-  auto fits = [&](int ns, int64_t lim) { return (slice + G::CE / ns - 1) / (G::CE / ns) <= lim; };
-  if ((forced == 1 || forced == 2 || forced == 4) && fits(forced, kMaxChunks)) return forced;
-  for (int ns : {4, 2})
-    if (fits(ns, kStore / 2)) return ns;
+  auto subs = [&](int ns) { return (slice + G::CE / ns - 1) / (G::CE / ns); };
+  if ((forced == 1 || forced == 2 || forced == 4) && subs(forced) <= kMaxChunks) return forced;
+  if (subs(4) <= 15) return 4;
+  if (subs(2) <= 15) return 2;
+  const double fill1 = static_cast<double>(slice) / static_cast<double>(subs(1) * G::CE);
+  if (subs(2) <= 17 && (ua || fill1 < 0.95)) return 2;
   return 1;
 }
 
 template <typename T, bool XP>
 int launch_streams(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
-  switch (pick_streams<T>(slice)) {
+  switch (pick_streams<T>(slice, false)) {
     case 4: return launch_c<T, 1, XP, false, 4>(a, slice, s, info);
     case 2: return launch_c<T, 1, XP, false, 2>(a, slice, s, info);
   }
@@ -1615,7 +1622,7 @@ int launch_t(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
   if (ua) {
     if ((a.V + G::EV - 1 + G::CE - 1) / G::CE > kMaxChunks) return -2;
-    switch (pick_streams<T>(a.V + G::EV - 1)) {  // a row spans up to EV - 1 more elements
+    switch (pick_streams<T>(a.V + G::EV - 1, true)) {  // a row spans up to EV - 1 more elements
       case 4: return launch_c<T, 1, false, true, 4>(a, a.V, s, info);
       case 2: return launch_c<T, 1, false, true, 2>(a, a.V, s, info);
     }
