@@ -81,7 +81,9 @@ def full(tag):
 
 
 EXTRA = [  # (capture name in gpurun_out or profiles, what, command)
-    ("r2_narrow18992", "fused loss on 18,992-wide rows (a P = 8 vocab shard), 16,384 rows bf16",
+    ("r2_narrow18992_ns4", "fused loss on 18,992-wide rows (a P = 8 vocab shard), 16,384 rows bf16, 4 row streams",
+     "ncu --set full -k regex:loss_tmem_kernel -s 3 -c 1 python scripts/narrow_rows.py 16384 18992"),
+    ("r2_narrow18992", "fused loss on 18,992-wide rows, one row at a time (before row streams; for comparison)",
      "scripts/ncu_narrow.sh (python scripts/narrow_rows.py 16384 18992)"),
     ("r2_wide151936", "fused loss on Qwen3 rows, 16,384 x 151,936 bf16 (isolated launch)",
      "scripts/ncu_narrow.sh (python scripts/narrow_rows.py 16384 151936)"),
