@@ -1228,6 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int jt = static_cast<int>(rsc.town & 0xffu);
       // dlogits rows share the logits rows' sector phase (checked at dispatch)
       T* drow = static_cast<T*>(a.dlogits) + t * a.ld_d + slice_start - mis;
+      T* const dlane = drow + EV * sid;  // this thread's first vector of chunk 0 (full chunks add k * SCE)
       const uint32_t sgn = neg ? 0x80008000u : 0u;
       const float gts = neg ? -gt : gt;  // target term before the sign flip
       // One chunk of dlogits. MODE (row-uniform): 0 = bf16 with |c0| folded
@@ -1323,8 +1324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           p1.z = pack_bf16x2(gr[12], gr[13]) ^ sgn;
           p1.w = pack_bf16x2(gr[14], gr[15]) ^ sgn;
           if (!partial) {
-            stg128_cs(dst + EV * sid, p0);
-            stg128_cs(dst + SHALF + EV * sid, p1);
+            T* const dv = dlane + k * SCE;
+            stg128_cs(dv, p0);
+            stg128_cs(dv + SHALF, p1);
           } else {
             // vector-granular tail (see the forward's partial chunk)
             const bool s0 = EV * sid < rem, s1 = SHALF + EV * sid < rem;
@@ -1381,8 +1383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       general_store:
         if (!partial) {
-          store_vec(dst + EV * sid, gr);
-          store_vec(dst + SHALF + EV * sid, gr + EV);
+          T* const dv = dlane + k * SCE;
+          store_vec(dv, gr);
+          store_vec(dv + SHALF, gr + EV);
         } else if (UA) {
           // front/tail chunk of an unaligned row: whole vectors where they are
           // entirely inside the row, element stores on the boundary vectors
