@@ -321,8 +321,10 @@ int sf_tm_vp_fused_loss_fwd_bwd(sf_tm_t h, const void* logits_shard, int32_t dty
                                 float* out_logp, float* out_entropy, void* stream);
 
 /* The checks sf_tm_vp_fused_loss_fwd_bwd makes on its shard (mailboxes open
- * and healthy, dtype, 16-B aligned rows/widths/strides, shard row fits one
- * CTA's row store), with no side effect. Ok or ConfigError / Internal. */
+ * and healthy, dtype, element-aligned rows with the dlogits rows at the logits
+ * rows' 16-B phase — an odd shard width or stride runs in 16-B sector
+ * coordinates —, shard row fits one CTA's row store), with no side effect.
+ * Ok or ConfigError / Internal. */
 int sf_tm_vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T, int64_t Vp, int64_t ld,
                          const void* dlogits, int64_t ld_d);
 

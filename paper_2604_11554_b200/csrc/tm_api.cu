@@ -307,10 +307,15 @@ int vp_fused_check(sf_tm_t h, const void* logits_shard, int32_t dtype, int64_t T
   if (bad_dtype(dtype)) return fail(h, SF_TM_CONFIG_ERROR, "dtype must be SF_TM_F32 or SF_TM_BF16");
   if (T < 0 || Vp <= 0 || ld < Vp || ld_d < Vp) return fail(h, SF_TM_CONFIG_ERROR, "bad shard shape or stride");
   const int64_t es = dtype == SF_TM_BF16 ? 2 : 4;
-  if ((reinterpret_cast<uintptr_t>(logits_shard) | reinterpret_cast<uintptr_t>(dlogits)) % 16 ||
-      (ld * es) % 16 || (ld_d * es) % 16 || (Vp * es) % 16)
-    return fail(h, SF_TM_CONFIG_ERROR, "fused vocab-parallel needs 16-B aligned shard rows, widths and strides");
-  if (!sftm::loss_xp_eligible(dtype, Vp))
+  const uintptr_t lb = reinterpret_cast<uintptr_t>(logits_shard), db = reinterpret_cast<uintptr_t>(dlogits);
+  // Rows off 16-B boundaries (an odd shard width or stride) run in sector
+  // coordinates, which needs the dlogits rows at the same 16-B phase as the
+  // logits rows (same base phase, stride difference a multiple of 16 B).
+  if (lb % es || db % es || (lb % 16) != (db % 16) || ((ld_d - ld) * es) % 16)
+    return fail(h, SF_TM_CONFIG_ERROR,
+                "fused vocab-parallel needs element-aligned shard rows with dlogits at the logits' 16-B phase");
+  const bool ua = (lb % 16) || (ld * es) % 16 || (Vp * es) % 16;
+  if (!sftm::loss_xp_eligible(dtype, Vp, ua))
     return fail(h, SF_TM_CONFIG_ERROR, "shard row too wide for the fused vocab-parallel kernel");
   return SF_TM_OK;
 }

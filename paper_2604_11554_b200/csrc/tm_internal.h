@@ -111,7 +111,7 @@ int launch_rows(const RowArgs& a, int mode, cudaStream_t s, std::string* err, La
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info);
 // Whether a shard row of Vp elements fits one CTA's row store (the fused
 // vocab-parallel kernel runs one CTA per row per rank).
-bool loss_xp_eligible(int dtype, int64_t Vp);
+bool loss_xp_eligible(int dtype, int64_t Vp, bool unaligned);
 // Forward-only streaming pass (kModeFwd / kModeVpStats) on 16-B aligned rows (tm_fwd.cu).
 int launch_fwd_stream(const RowArgs& a, int mode, cudaStream_t s, LaunchInfo* info);
 

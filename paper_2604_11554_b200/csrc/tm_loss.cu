@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // stores, 8 = no TMEM traffic. Compile-time, so the product build carries none of it.
   constexpr int dbg_mode = SFTM_DBG_MODE;
   static_assert(!XP || C == 1, "peer exchange runs one CTA per row per rank");
-  static_assert(!UA || (C == 1 && !XP), "unaligned rows run one CTA per row");
+  static_assert(!UA || C == 1, "unaligned rows run one CTA per row");
   static_assert(NS == 1 || C == 1, "row streams: one CTA per row slice");
   static_assert(NS == 1 || NS == 2 || NS == 4, "row streams");
   using G = Geo<T>;
@@ -1652,22 +1652,31 @@ int launch_loss_tmem(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
   return loss::launch_t<float>(a, s, info);
 }
 
-bool loss_xp_eligible(int dtype, int64_t Vp) {
+bool loss_xp_eligible(int dtype, int64_t Vp, bool ua) {
+  // one CTA per row per rank: the whole shard row (in sector coordinates if
+  // unaligned) must fit the row store
   auto fits = [&](auto tag) {
     using G = loss::Geo<decltype(tag)>;
-    const int64_t slice = (Vp + G::EV - 1) / G::EV * G::EV;
-    return (slice + G::CE - 1) / G::CE <= loss::kMaxChunks;
+    const int64_t span = ua ? Vp + G::EV - 1 : (Vp + G::EV - 1) / G::EV * G::EV;
+    return (span + G::CE - 1) / G::CE <= loss::kMaxChunks;
   };
   return dtype == 1 ? fits(uint16_t{}) : fits(float{});
 }
 
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
-  // one CTA per row per rank: the whole shard row slice must fit the row store
   auto go = [&](auto tag) -> int {
     using T = decltype(tag);
     using G = loss::Geo<T>;
-    int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
-    if ((slice + G::CE - 1) / G::CE > loss::kMaxChunks) return -2;
+    const bool ua = (reinterpret_cast<uintptr_t>(a.logits) % 16) || ((a.ld * G::es) % 16) || ((a.V * G::es) % 16);
+    if (!loss_xp_eligible(a.dtype, a.V, ua)) return -2;
+    if (ua) {  // an odd shard width or stride: sector coordinates (the caller checked the dlogits phase)
+      switch (loss::pick_streams<T>(a.V + G::EV - 1, true)) {
+        case 4: return loss::launch_c<T, 1, true, true, 4>(a, a.V, s, info);
+        case 2: return loss::launch_c<T, 1, true, true, 2>(a, a.V, s, info);
+      }
+      return loss::launch_c<T, 1, true, true, 1>(a, a.V, s, info);
+    }
+    const int64_t slice = (a.V + G::EV - 1) / G::EV * G::EV;
     return loss::launch_streams<T, true>(a, slice, s, info);
   };
   if (a.dtype == 1) return go(uint16_t{});

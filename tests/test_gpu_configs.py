@@ -61,7 +61,11 @@ def _vp_group(tm, P):
 
 @pytest.mark.parametrize("P,dtype,V,pkw", [(1, "bf16", 151936, {}), (1, "f32", 32000, {"kl_beta": 0.05}),
                                            (2, "bf16", 151936, {"entropy_coef": 0.01}), (4, "bf16", 151936, {}),
-                                           (8, "bf16", 151936, {"kl_beta": 0.05}), (2, "f32", 32000, {})])
+                                           (8, "bf16", 151936, {"kl_beta": 0.05}), (2, "f32", 32000, {}),
+                                           # odd vocabularies: the last shard's rows are off 16-B boundaries
+                                           # (sector coordinates) while the others are aligned
+                                           (4, "bf16", 50257, {"entropy_coef": 0.01}), (8, "bf16", 50257, {}),
+                                           (2, "f32", 32001, {"kl_beta": 0.05})])
 def test_vp_fused_emulated_ranks(tm, orc, P, dtype, V, pkw):
     from paper_2604_11554_b200 import _lib
     from paper_2604_11554_b200.vocab_parallel import shard_bounds
