@@ -295,7 +295,7 @@ def run_vocab_parallel(args, world, rank, dev, dist):
     from paper_2604_11554_b200 import _lib, seam, train_math as tm
     from paper_2604_11554_b200.vocab_parallel import gather_stats, open_peer_exchange, shard_bounds
 
-    V, P = 151936, world
+    V, P = args.vocab, world  # Qwen3's 151,936 unless --vocab (e.g. an odd vocabulary's last shard)
     b = shard_bounds(V, P)
     vs, Vp = b[rank], b[rank + 1] - b[rank]
     prompts, G, Ls, S = 256, 16, 1024, 128

@@ -865,6 +865,7 @@ int sf_tm_vp_mailbox_open(sf_tm_t h, const void* ipc_handles) {
       return check_cuda(h, e, "sf_tm_vp_mailbox_open (cudaIpcOpenMemHandle)");
     }
   }
+  if (const int e = sftm::prepare_loss_xp()) return check_cuda(h, static_cast<cudaError_t>(e), "sf_tm_vp_mailbox_open");
   h->xp_ready = true;
   return SF_TM_OK;
 }
@@ -952,6 +953,8 @@ int sf_tm_debug_vp_local_group(sf_tm_t* handles, int32_t P, int32_t grid_per_ran
     if (int rc = use_device(handles[r])) return rc;
     if (int rc = alloc_mailbox(handles[r], P, r)) return rc;
   }
+  if (const int e = sftm::prepare_loss_xp())
+    return check_cuda(handles[0], static_cast<cudaError_t>(e), "sf_tm_debug_vp_local_group");
   for (int r = 0; r < P; ++r) {
     sf_tm_t h = handles[r];
     for (int q = 0; q < P; ++q) h->xp_mail[q] = handles[q]->xp_local;

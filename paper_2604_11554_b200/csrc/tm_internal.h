@@ -112,6 +112,10 @@ int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info);
 // Whether a shard row of Vp elements fits one CTA's row store (the fused
 // vocab-parallel kernel runs one CTA per row per rank).
 bool loss_xp_eligible(int dtype, int64_t Vp, bool unaligned);
+// One-time setup of every peer-exchange kernel instantiation on the current
+// device (called when the mailboxes are wired, before any rank can be waiting
+// in a launch). Returns a cudaError_t value.
+int prepare_loss_xp();
 // Forward-only streaming pass (kModeFwd / kModeVpStats) on 16-B aligned rows (tm_fwd.cu).
 int launch_fwd_stream(const RowArgs& a, int mode, cudaStream_t s, LaunchInfo* info);
 

@@ -374,21 +374,25 @@ struct RowSeq {
 #ifdef SFTM_HANG_DEBUG
 // Debug build only (EXTRA=-DSFTM_HANG_DEBUG, scripts/hang_debug.py): a wait that
 // gives up after 2 s and records where, so a protocol deadlock shows its
-// waiting sites instead of hanging the GPU. dbg[0]: the first give-up (line |
-// parity << 16 | barrier offset << 20 | CTA << 40 | warp << 56); dbg[16 + 32 *
-// CTA + warp]: each warp's first give-up; dbg[15]: abort flag (later waits give
-// up at once).
-__device__ __forceinline__ void kwait(unsigned long long* dbg, int line, uint32_t bar, uint32_t par) {
+// waiting sites instead of hanging the GPU. Records (host-mapped memory, so
+// they survive a fault): line | parity << 16 | rank << 20 | row << 24 |
+// CTA << 40 | warp << 56; dbg[0] the first give-up, dbg[16 + (rank * 148 +
+// CTA) * 32 + warp] each warp's first; dbg[15] the abort flag (later waits give
+// up at once). `row` is the warp's active-row counter (dbg_row).
+__device__ __forceinline__ void kwait(unsigned long long* dbg, int line, uint32_t bar, uint32_t par, int rank,
+                                      uint32_t row) {
   if (mbar_try_wait(bar, par)) return;
   volatile unsigned long long* vd = dbg;  // host-mapped (pinned) memory: readable after a fault
   const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(bar, par)) {
     if (vd[15] != 0ull || globaltimer_ns() - t0 > 2000000000ull) {
       const unsigned long long rec = static_cast<unsigned long long>(line) | (static_cast<unsigned long long>(par) << 16) |
-                                     (static_cast<unsigned long long>(bar & 0xffffu) << 20) |
-                                     (static_cast<unsigned long long>(blockIdx.x) << 40) |
+                                     (static_cast<unsigned long long>(rank & 15) << 20) |
+                                     (static_cast<unsigned long long>(row & 0xffffu) << 24) |
+                                     (static_cast<unsigned long long>(blockIdx.x & 0xffu) << 40) |
                                      (static_cast<unsigned long long>(threadIdx.x >> 5) << 56);
-      if (vd[16 + blockIdx.x * 32 + (threadIdx.x >> 5)] == 0ull) vd[16 + blockIdx.x * 32 + (threadIdx.x >> 5)] = rec;
+      const size_t i = 16 + (static_cast<size_t>(rank & 7) * 148 + blockIdx.x) * 32 + (threadIdx.x >> 5);
+      if (vd[i] == 0ull) vd[i] = rec;
       if (vd[15] == 0ull) vd[0] = rec;
       vd[15] = 1ull;
       __threadfence_system();
@@ -396,9 +400,11 @@ __device__ __forceinline__ void kwait(unsigned long long* dbg, int line, uint32_
     }
   }
 }
-#define KWAIT(bar, par) kwait(a.dbg, __LINE__, bar, par)
+#define KWAIT(bar, par) kwait(a.dbg, __LINE__, bar, par, a.xp_rank, dbg_row)
+#define DBG_ROW(n) (dbg_row = (n))
 #else
 #define KWAIT(bar, par) mbar_wait(bar, par)
+#define DBG_ROW(n) ((void)0)
 #endif
 
 template <typename T, int C, bool XP = false, bool UA = false, int NS = 1>
@@ -441,6 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+#ifdef SFTM_HANG_DEBUG
+  uint32_t dbg_row = 0;
+#endif
   const uint32_t crank = (C > 1) ? cluster_ctarank() : 0u;
   const int64_t cid = (C > 1) ? static_cast<int64_t>(cluster_id_x()) : blockIdx.x;
   const int64_t ncl = (C > 1) ? static_cast<int64_t>(nclusters_x()) : gridDim.x;
@@ -697,6 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (rows.next(t)) {
       if (NS > 1 && static_cast<int>(nrow % NS) != sg) {  // another stream's row
         ++nrow;
+        DBG_ROW(nrow);
         continue;
       }
       const int mis = row_mis(t);
@@ -901,6 +911,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(smem_u32(&red_bar[nrow % RD]));
       }
       ++nrow;
+      DBG_ROW(nrow);
     }
     // the CTA's last group of rows has no row for this stream: idle through its steps
     if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS))
@@ -965,6 +976,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             XpMsg* dst = static_cast<XpMsg*>(a.xp_mail[lane]) + xp_index(a.xp_epoch, static_cast<int>(cid), mb, a.xp_rank);
             st_sys_v2u64(&dst->w[0], tag | __float_as_uint(v.m2), tag | __float_as_uint(v.s));
             st_sys_v2u64(&dst->w[2], tag | __float_as_uint(v.w), tag | __float_as_uint(zy));
+#ifdef SFTM_HANG_DEBUG
+            if (lane == 0)  // the sender's progress: rows posted, epoch, and the address for peer 0 (hang_debug)
+              reinterpret_cast<volatile unsigned long long*>(a.dbg)[16 + 2 * 8 * 148 * 32 + (a.xp_rank & 7) * 148 +
+                                                                    blockIdx.x] =
+                  (nrow + 1) | (static_cast<unsigned long long>(a.xp_epoch & 0xff) << 8) |
+                  (static_cast<unsigned long long>(reinterpret_cast<uintptr_t>(
+                       static_cast<XpMsg*>(a.xp_mail[0]) + xp_index(a.xp_epoch, static_cast<int>(cid), mb, a.xp_rank)) &
+                                                   0xffffffffull)
+                   << 16);
+            if (lane == 0 && nrow < 4)
+              reinterpret_cast<volatile unsigned long long*>(a.dbg)[16 + 2 * 8 * 148 * 32 + 8 * 148 +
+                                                                    ((a.xp_rank & 7) * 148 + blockIdx.x) * 4 + nrow] =
+                  globaltimer_ns();
+#endif
           }
         } else if (static_cast<int>(nrow % (kNCtl - 1)) == ci - 1) {
           // ------------------------------------------------ receivers (rows alternate)
@@ -989,6 +1014,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // word, surfaced by the next API call as Internal) and let the
                 // kernel run to completion on the stale mailbox values.
                 const uint64_t el = globaltimer_ns() - t0;
+#ifdef SFTM_HANG_DEBUG
+                if (el > 1000000000ull) {  // which peer's message of which row is late (hang_debug)
+                  volatile unsigned long long* vd = a.dbg + 16 + 8 * 148 * 32;
+                  const size_t i = (static_cast<size_t>(a.xp_rank & 7) * 148 + blockIdx.x) * 32 + lane;
+                  if (vd[i] == 0ull)
+                    vd[i] = (static_cast<unsigned long long>(nrow & 0xff) << 56) | (a.xp_epoch & 0xff) << 48 |
+                            (reinterpret_cast<uintptr_t>(src) & 0xffffffffull) << 8 | 1ull;
+                  vd[8 * 148 * 32 + 8 * 148 + 8 * 148 * 4 + i] = t0;  // when this receiver started waiting
+                }
+#endif
                 if (el > 1000000ull &&
                     (el > a.xp_timeout_ns || *reinterpret_cast<volatile int*>(a.xp_abort) != 0)) {
                   atomicExch(a.xp_abort, 1);
@@ -1042,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         ++nrow;
+        DBG_ROW(nrow);
         }
       }
     } else {
@@ -1057,6 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (bits != 0u && static_cast<int>(nrow % kNCtl) != ci) {
         bits &= bits - 1u;
         ++nrow;
+        DBG_ROW(nrow);
       }
       while (bits != 0u) {
       const int i = __ffs(bits) - 1;
@@ -1147,10 +1184,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     
       ++nrow;
+      DBG_ROW(nrow);
       // skip to this warp's next row (kNCtl - 1 rows of the other control warps)
       for (int q = 1; q < kNCtl && bits != 0u; ++q) {
         bits &= bits - 1u;
         ++nrow;
+        DBG_ROW(nrow);
       }
       }
       // rows of this window past our last one belong to the others: nrow already
@@ -1213,6 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (NS > 1 && static_cast<int>(nrow % NS) != sg) {  // another stream's row
         ++nrow;
+        DBG_ROW(nrow);
         continue;
       }
       const int mis = row_mis(t);
@@ -1463,6 +1503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&scal_free[rs]));
       ++nrow;
+      DBG_ROW(nrow);
     }
     // the CTA's last group of rows has no row for this stream: idle through its steps
     if (NS > 1 && static_cast<int>(nrow % NS) != 0 && sg >= static_cast<int>(nrow % NS)) {
@@ -1494,16 +1535,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 std::mutex g_mu;
 
+// One-time setup of an instantiation on the current device (dynamic smem
+// opt-in, occupancy): returns the co-resident CTA (cluster) count, or < 0 with
+// *err. cudaFuncSetAttribute can wait for kernels already running, so the
+// peer-exchange instantiations are prepared when the mailboxes are wired
+// (prepare_loss_xp), never while a peer's kernel spins waiting for this one.
 template <typename T, int C, bool XP = false, bool UA = false, int NS = 1>
-int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
+int init_c(cudaError_t* err) {
   auto kern = loss_tmem_kernel<T, C, XP, UA, NS>;
   static PerDevice cache;  // per instantiation and device
   int& max_active = cache();
+  *err = cudaSuccess;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (max_active < 0) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
-      if (e != cudaSuccess) return e;
+      if (e != cudaSuccess) {
+          *err = e;
+          return -1;
+        }
       if (C > 1) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C * 256);
@@ -1518,19 +1568,37 @@ int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) 
         cfg.numAttrs = 1;
         int n = 0;
         e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {
+          *err = e;
+          return -1;
+        }
         max_active = n;
       } else {
         int per_sm = 0, dev = 0, sms = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kRingBytes);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {
+          *err = e;
+          return -1;
+        }
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         max_active = per_sm * sms;
       }
-      if (max_active <= 0) return cudaErrorInvalidConfiguration;
+      if (max_active <= 0) {
+        *err = cudaErrorInvalidConfiguration;
+        return -1;
+      }
     }
   }
+  return max_active;
+}
+
+template <typename T, int C, bool XP = false, bool UA = false, int NS = 1>
+int launch_c(const RowArgs& a, int64_t slice, cudaStream_t s, LaunchInfo* info) {
+  auto kern = loss_tmem_kernel<T, C, XP, UA, NS>;
+  cudaError_t ie;
+  const int max_active = init_c<T, C, XP, UA, NS>(&ie);
+  if (max_active < 0) return ie;
   int64_t ncl = a.T < max_active ? a.T : max_active;
   if (XP) {  // same grid on every rank, whatever T
     ncl = max_active < kXpMaxCtas ? max_active : kXpMaxCtas;
@@ -1661,6 +1729,26 @@ bool loss_xp_eligible(int dtype, int64_t Vp, bool ua) {
     return (span + G::CE - 1) / G::CE <= loss::kMaxChunks;
   };
   return dtype == 1 ? fits(uint16_t{}) : fits(float{});
+}
+
+int prepare_loss_xp() {
+  cudaError_t e = cudaSuccess, ie = cudaSuccess;
+  auto one = [&](int r) {
+    if (r < 0 && e == cudaSuccess) e = ie;
+  };
+  one(loss::init_c<uint16_t, 1, true, false, 1>(&ie));
+  one(loss::init_c<uint16_t, 1, true, false, 2>(&ie));
+  one(loss::init_c<uint16_t, 1, true, false, 4>(&ie));
+  one(loss::init_c<uint16_t, 1, true, true, 1>(&ie));
+  one(loss::init_c<uint16_t, 1, true, true, 2>(&ie));
+  one(loss::init_c<uint16_t, 1, true, true, 4>(&ie));
+  one(loss::init_c<float, 1, true, false, 1>(&ie));
+  one(loss::init_c<float, 1, true, false, 2>(&ie));
+  one(loss::init_c<float, 1, true, false, 4>(&ie));
+  one(loss::init_c<float, 1, true, true, 1>(&ie));
+  one(loss::init_c<float, 1, true, true, 2>(&ie));
+  one(loss::init_c<float, 1, true, true, 4>(&ie));
+  return e;
 }
 
 int launch_loss_xp(const RowArgs& a, cudaStream_t s, LaunchInfo* info) {
