@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       if constexpr (UA) {
-        // peeled like the aligned schedule: only the front and tail chunks are masked
+        // peeled like the aligned schedule: only the front and tail chunks are
+        // masked (one masked copy for every chunk measured 25-30% slower)
         const int nfull_r = span / SCE;
         if (nck_r > 0) {
           if (mis > 0 || span < SCE) {
@@ -1457,25 +1458,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       const int mode = (G::es == 2 && c1 == 0.f) ? 0 : (c1 == 0.f ? 1 : 2);
       if constexpr (UA) {
-        const int nfull_r = span / SCE;
-        const bool front = mis > 0 || span < SCE;
+        // bf16 rows take mode 0 or 2, fp32 rows 1 or 2: only those schedules are
+        // instantiated, and a full chunk 0 runs as the loop's first step. The
+        // unaligned kernel's code size is what its narrow rows pay for in
+        // instruction-cache misses (ncu at 12,569-wide rows: no_instruction
+        // stalls 2.8 per issue vs 0.5 aligned); this trim: +12% there.
         auto sched = [&](auto md) {
           constexpr int M = decltype(md)::value;
+          const int nfull_r = span / SCE;
+          const bool front = mis > 0 || span < SCE;
           if (nck_r == 0) return;
-          if (front) {
-            bchunk(0, true, M);
-          } else {
-            bchunk(0, false, M);
-          }
-          for (int k = 1; k < nfull_r; ++k) bchunk(k, false, M);
+          if (front) bchunk(0, true, M);
+          for (int k = front ? 1 : 0; k < nfull_r; ++k) bchunk(k, false, M);
           if (nck_r > nfull_r && nck_r > 1) bchunk(nck_r - 1, true, M);
         };
-        if (mode == 0) {
-          sched(std::integral_constant<int, 0>{});
-        } else if (mode == 1) {
-          sched(std::integral_constant<int, 1>{});
+        if constexpr (G::es == 2) {
+          if (mode == 0) {
+            sched(std::integral_constant<int, 0>{});
+          } else {
+            sched(std::integral_constant<int, 2>{});
+          }
         } else {
-          sched(std::integral_constant<int, 2>{});
+          if (mode == 1) {
+            sched(std::integral_constant<int, 1>{});
+          } else {
+            sched(std::integral_constant<int, 2>{});
+          }
         }
       } else if (mode == 0) {
         for (int k = 0; k < nfull; ++k) bchunk(k, false, 0);
