@@ -203,7 +203,9 @@ int sf_tm_token_weights(sf_tm_t h, const int32_t* cu_seqlens, int64_t B, const f
  * kernel when dlogits rows sit at the same 16-byte phase as the logits rows
  * (same base alignment mod 16, stride difference a multiple of 16 bytes) and
  * a row slice fits the row store; otherwise a two-pass kernel computes the
- * same outputs. sf_tm_last_launch reports which ran. */
+ * same outputs. Narrow rows (a row taking a few 12 KB chunks, e.g. a
+ * vocab-parallel shard) run 2 or 4 rows side by side per CTA ("row streams").
+ * sf_tm_last_launch / sf_tm_last_launch_streams report which ran. */
 int sf_tm_pg_loss_fwd_bwd(sf_tm_t h, const void* logits, int32_t dtype, int64_t T, int64_t V,
                           int64_t ld, const int32_t* targets, const float* old_logp,
                           const float* ref_logp, const float* adv_tok, const float* w_tok,
