@@ -57,8 +57,12 @@ namespace loss {
 #define SFTM_DBG_MODE 0
 #endif
 
-constexpr int kFW = 12;                     // forward warps (3 per SM sub-partition)
-constexpr int kBW = 12;                     // backward warps (3 per SM sub-partition)
+#ifndef SFTM_FW
+#define SFTM_FW 12
+#endif
+constexpr int kFW = SFTM_FW;                // forward warps (3 per SM sub-partition)
+constexpr int kBW = SFTM_FW;                // backward warps (3 per SM sub-partition)
+static_assert(kFW % 4 == 0, "forward / backward warps come in SM sub-partition quads");
 constexpr int kFT = kFW * 32;               // 384 forward threads
 constexpr int kProd = kFW + kBW;            // producer warp index
 constexpr int kCtl = kFW + kBW + 1;         // control warps (2, alternating rows): merge, exchange, scalars
@@ -73,7 +77,7 @@ constexpr int kCB = kFT * 32;               // chunk bytes: two 16-B vectors per
 #define SFTM_RING_SLOTS 8
 #endif
 constexpr int kSlots = SFTM_RING_SLOTS;     // TMA landing ring slots (96 KB)
-constexpr int kSSlots = 18 - kSlots;        // shared-memory row-store slots (120 KB)
+constexpr int kSSlots = (216 * 1024) / kCB - kSlots;  // shared-memory row-store slots (120 KB)
 constexpr int kRingBytes = (kSlots + kSSlots) * kCB;  // dynamic smem: ring + smem row store
 constexpr int kSlotCols = kCB / (128 * 4);  // TMEM columns per chunk slot (24)
 constexpr int kTSlots = 512 / kSlotCols;    // 21 TMEM chunk slots (252 KB)
