@@ -37,6 +37,14 @@
 // released only after the values read from it fed a dependent instruction
 // (SASS issues an mbarrier arrive right behind an LDS without waiting for it).
 //
+// Narrow rows (a vocab-parallel shard) run NS = 2 or 4 ROW STREAMS: the warp
+// pairs split into NS groups, consecutive loss-active rows go to the groups in
+// turn, and each ring / row-store slot carries one sub-chunk of every group's
+// row, so the per-row work is paid NS times less often per SM (see the kernel
+// comment; the control warps then hand rows off strictly in row order). Rows
+// are found 32 at a time by a ballot over their weights, and the control warps
+// hold a 32-row window of per-row inputs, one row per lane.
+//
 // Reference seam replaced: trainer_compute_batch latency (proj/src/sim_runtime.cpp:441)
 // and trainer_thread sleep (proj/src/wall_runtime.cpp:197); math pinned in
 // DESIGN.md §2, fp64 twin oracle/sf_oracle.c orc_pg_loss_fwd_bwd.
