@@ -308,6 +308,35 @@ def test_pg_loss_deterministic(tm, orc):
     assert np.array_equal(d1, d2)
 
 
+def test_vocab_padding_columns_are_inert(tm, orc):
+    """padding an odd vocabulary to a multiple of 8 * P with a
+    large finite negative logit (-1e4) leaves logp, entropy, the metrics and the
+    real columns' dlogits unchanged and gives the padding columns dlogits of
+    exactly 0 (their probability underflows to 0; no repair path)."""
+    from paper_2604_11554_b200 import _lib
+
+    V, Vpad = 50257, 50272
+    prob = orc.synth_problem(41, [33, 20, 51], V, "bf16", prompt_max=8)
+    T = prob["T"]
+    logits = to_dev_logits(prob)
+    padded = torch.full((T, Vpad), -1e4, dtype=torch.bfloat16, device="cuda")
+    padded[:, :V] = logits
+    cu, sid, mask, adv, adv_tok, w_tok = gpu_pipeline(tm, prob, 0)
+    params = _lib.default_loss_params(kl_beta=0.05, entropy_coef=0.01)
+    args = (i32(prob["targets"]), f32(prob["old"]), f32(prob["ref"]), adv_tok, w_tok, params)
+    m0, d0, lp0, e0 = tm.pg_loss_fwd_bwd(logits, *args, want_logp=True)
+    m1, d1, lp1, e1 = tm.pg_loss_fwd_bwd(padded, *args, want_logp=True)
+    torch.cuda.synchronize()
+    assert tm.handle().last_launch()["kernel"] == "loss_tmem_kernel"
+    assert torch.all(d1[:, V:] == 0)
+    act = w_tok != 0
+    assert torch.allclose(lp1[act], lp0[act], atol=2e-6, rtol=2e-6)
+    assert torch.allclose(e1[act], e0[act], atol=2e-5, rtol=2e-5)
+    assert torch.allclose(m1[:6], m0[:6], atol=2e-6, rtol=2e-5)
+    g0, g1 = d0.float(), d1[:, :V].float()
+    assert torch.all((g1 - g0).abs() <= 2.0 ** -7 * g0.abs() + 1e-9)
+
+
 @pytest.mark.parametrize("dtype,V", [("bf16", 3000), ("f32", 5000)])
 def test_pg_loss_deep_runahead(tm, orc, dtype, V):
     """Many short rows: a row slice is one chunk, so the forward warps can run
